@@ -1,0 +1,98 @@
+"""ctypes binding of the C ABI (include/rinr_b200.h) exported by the in-tree
+``_lib/librinr_b200.so``.  There is no fallback: if the library is missing the
+import fails loudly (build it with ``python -m paper_2306_16699_b200.build``)."""
+
+from __future__ import annotations
+
+import ctypes as C
+from pathlib import Path
+
+from .errors import raise_for_status
+
+LIB_PATH = Path(__file__).resolve().parent / "_lib" / "librinr_b200.so"
+
+# enums (include/rinr_b200.h)
+OUT_F32, OUT_BF16, OUT_U8 = 0, 1, 2
+LAYOUT_NCHW, LAYOUT_NHWC = 0, 1
+PREC_FP32, PREC_BF16, PREC_EXACT = 0, 1, 2
+SIN_MUFU, SIN_ACCURATE = 0, 1
+AUG_NONE, AUG_OFFSET, AUG_CROP = 0, 1, 2
+
+EXPORTS = (
+    "rinr_abi_version", "rinr_last_error", "rinr_last_error_record", "rinr_archive_validate",
+    "rinr_store_create", "rinr_store_destroy", "rinr_store_info", "rinr_store_record_meta",
+    "rinr_dequantize", "rinr_decode",
+)
+
+
+class StoreInfo(C.Structure):
+    _fields_ = [
+        ("num_records", C.c_int64), ("total_records", C.c_int64),
+        ("shard_rank", C.c_uint32), ("shard_world", C.c_uint32),
+        ("device", C.c_int32), ("uniform_arch", C.c_int32), ("n_dims", C.c_int32),
+        ("dims", C.c_uint16 * 32), ("omega", C.c_double),
+        ("max_param_count", C.c_int64), ("max_record_bytes", C.c_int64), ("device_bytes", C.c_int64),
+        ("uniform_source", C.c_int32), ("source_h", C.c_uint32), ("source_w", C.c_uint32),
+    ]
+
+
+class DecodeParams(C.Structure):
+    _fields_ = [
+        ("out_h", C.c_int32), ("out_w", C.c_int32), ("out_dtype", C.c_int32), ("out_layout", C.c_int32),
+        ("precision", C.c_int32), ("sin_mode", C.c_int32), ("aug_mode", C.c_int32),
+        ("mean", C.c_float * 3), ("std", C.c_float * 3),
+    ]
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not LIB_PATH.exists():
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_2306_16699_b200.build` "
+                          "(there is no CPU fallback)")
+    L = C.CDLL(str(LIB_PATH))
+    vp, i64, i32p = C.c_void_p, C.c_int64, C.POINTER(C.c_int32)
+    L.rinr_abi_version.restype = C.c_int
+    L.rinr_last_error.restype = C.c_char_p
+    L.rinr_last_error_record.restype = i64
+    L.rinr_archive_validate.argtypes = [vp, C.c_size_t, C.POINTER(i64)]
+    L.rinr_store_create.argtypes = [vp, C.c_size_t, C.c_int, C.c_uint32, C.c_uint32, C.POINTER(vp)]
+    L.rinr_store_destroy.argtypes = [vp]
+    L.rinr_store_info.argtypes = [vp, C.POINTER(StoreInfo)]
+    L.rinr_store_record_meta.argtypes = [vp, i64, C.POINTER(i64), C.c_char_p, C.c_size_t,
+                                         C.POINTER(C.c_size_t), C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]
+    L.rinr_dequantize.argtypes = [vp, vp, i64, vp, i64, vp, vp]
+    L.rinr_decode.argtypes = [vp, vp, i64, C.POINTER(DecodeParams), vp, vp, vp, vp]
+    for name in EXPORTS:
+        if name != "rinr_abi_version" and name not in ("rinr_last_error", "rinr_last_error_record"):
+            getattr(L, name).restype = C.c_int
+    if L.rinr_abi_version() != 1:
+        raise ImportError("librinr_b200.so ABI version mismatch")
+    _lib = L
+    return L
+
+
+def check(code: int) -> None:
+    if code != 0:
+        L = lib()
+        raise_for_status(code, L.rinr_last_error().decode("utf-8", "replace"), int(L.rinr_last_error_record()))
+
+
+def archive_validate(data: bytes) -> int:
+    """Host-only validation of an archive image; returns the record count."""
+    n = C.c_int64(0)
+    arr = host_view(data)
+    check(lib().rinr_archive_validate(arr.ctypes.data if arr.size else None, arr.size, C.byref(n)))
+    return n.value
+
+
+def host_view(data):
+    """Zero-copy uint8 view of bytes / bytearray / memoryview / numpy data."""
+    import numpy as np  # noqa: PLC0415
+    if isinstance(data, np.ndarray):
+        return np.ascontiguousarray(data).view(np.uint8).reshape(-1)
+    return np.frombuffer(data, dtype=np.uint8)

@@ -1,0 +1,212 @@
+// Device helpers shared by every kernel: unaligned reads of record bytes held
+// in shared memory, the per-layer section walk, the bit-exact integer
+// dequantisation (reference archive.py:278-325), coordinates
+// (net.py:138-149) and the fused epilogue (clamp / pad fill / normalise /
+// convert / store).
+#pragma once
+
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "rinr_internal.h"
+
+namespace rinr {
+
+// ---------------------------------------------------------------------------
+// Byte access into a 16-B aligned shared-memory copy of a record.  Fields in
+// the .rinr format are packed (no alignment), so 32-bit values are assembled
+// from the two aligned words that cover them.  Buffers are over-allocated by
+// 16 bytes so the second word is always in bounds.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t ld_u32u(const uint8_t* base, uint32_t off) {
+  const uint32_t* w = reinterpret_cast<const uint32_t*>(base + (off & ~3u));
+  uint32_t lo = w[0], hi = w[1];
+  return __funnelshift_r(lo, hi, (off & 3u) * 8u);
+}
+__device__ __forceinline__ uint32_t ld_u16u(const uint8_t* base, uint32_t off) { return ld_u32u(base, off) & 0xFFFFu; }
+__device__ __forceinline__ double ld_f64u(const uint8_t* base, uint32_t off) {
+  return __hiloint2double(int(ld_u32u(base, off + 4)), int(ld_u32u(base, off)));
+}
+
+// Copy `bytes` (multiple of 16, 16-B aligned source) from global to shared
+// memory with 16-B vector loads spread over `nthr` threads.
+__device__ __forceinline__ void copy_record(uint8_t* dst, const uint8_t* __restrict__ src, uint32_t bytes, int tid,
+                                            int nthr) {
+  const uint4* s = reinterpret_cast<const uint4*>(src);
+  uint4* d = reinterpret_cast<uint4*>(dst);
+  for (uint32_t i = tid; i < bytes / 16; i += nthr) d[i] = __ldg(s + i);
+}
+
+// One layer's sections, located from its tag offset and the next layer's
+// offset (bias is the last 4*out bytes of the section; archive.py:112-137).
+struct DLayer {
+  int tag, form, cst;
+  int in, out, n;
+  double scale;
+  int zp;
+  uint32_t bits_off, vals_off, bias_off;
+};
+
+__device__ __forceinline__ DLayer parse_layer(const uint8_t* rec, uint32_t off, uint32_t next_off, int in, int out) {
+  DLayer L;
+  uint32_t h = ld_u32u(rec, off);
+  L.tag = h & 0xFF;
+  L.form = (h >> 8) & 0xFF;
+  L.cst = (h >> 16) & 0xFF;
+  L.in = in;
+  L.out = out;
+  L.n = in * out;
+  uint32_t p = off + 3;
+  L.scale = 1.0;
+  L.zp = 0;
+  if (L.tag == TAG_A8 || L.tag == TAG_A16) {
+    L.scale = ld_f64u(rec, p);
+    L.zp = int(ld_u32u(rec, p + 8));
+    p += 12;
+  }
+  L.bits_off = p;
+  if (L.form != FORM_DENSE) p += (uint32_t(L.n) + 7) / 8;
+  L.vals_off = p;
+  L.bias_off = next_off - 4u * uint32_t(out);
+  return L;
+}
+
+// Word view of the kept-bitset (LSB-first, row-major; archive.py:122, 288-290)
+// plus exclusive popcount prefix per word, so the value index of a sparse
+// entry j is prefix[j/32] + popc(word[j/32] & ((1 << j%32) - 1)).  Built by
+// one warp; caller synchronises before use.
+__device__ __forceinline__ void build_bit_prefix(const uint8_t* rec, const DLayer& L, uint32_t* words,
+                                                 uint32_t* prefix, int lane) {
+  const int nw = (L.n + 31) / 32;
+  uint32_t carry = 0;
+  for (int base = 0; base < nw; base += 32) {
+    int w = base + lane;
+    uint32_t v = 0;
+    if (w < nw) {
+      v = ld_u32u(rec, L.bits_off + 4u * uint32_t(w));
+      int rem = L.n - 32 * w;
+      if (rem < 32) v &= (1u << rem) - 1u;  // bytes past the bitset belong to the values
+      words[w] = v;
+    }
+    uint32_t c = __popc(v), incl = c;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      uint32_t t = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += t;
+    }
+    if (w < nw) prefix[w] = carry + incl - c;
+    carry += __shfl_sync(0xffffffffu, incl, 31);
+  }
+}
+
+// Materialised weight entry j (row-major (out, in)) of layer L — bit-exact
+// with archive.materialize:
+//   affine, not const : kept ? f32(f64(scale) * (f64(code) - f64(zp))) : +0.0
+//   f32 / f16 / const : sparse ? (kept ? value : +0.0) : stored value
+__device__ __forceinline__ float dq_weight(const uint8_t* rec, const DLayer& L, const uint32_t* words,
+                                           const uint32_t* prefix, int j) {
+  bool kept = true;
+  int vi = j;
+  if (L.form != FORM_DENSE) {
+    uint32_t wd = words[j >> 5];
+    kept = (wd >> (j & 31)) & 1u;
+    if (L.form == FORM_SPARSE) vi = int(prefix[j >> 5] + __popc(wd & ((1u << (j & 31)) - 1u)));
+  }
+  const bool affine = L.tag == TAG_A8 || L.tag == TAG_A16;
+  if (affine && !L.cst) {
+    if (!kept) return 0.0f;
+    uint32_t code = L.tag == TAG_A8 ? uint32_t(rec[L.vals_off + vi]) : ld_u16u(rec, L.vals_off + 2u * vi);
+    double diff = double(code) - double(L.zp);  // exact: both are integers < 2^33
+    return __double2float_rn(__dmul_rn(L.scale, diff));
+  }
+  if (L.form == FORM_SPARSE && !kept) return 0.0f;
+  if (L.tag == TAG_F16) return __half2float(__ushort_as_half((unsigned short)ld_u16u(rec, L.vals_off + 2u * vi)));
+  return __uint_as_float(ld_u32u(rec, L.vals_off + 4u * vi));
+}
+
+__device__ __forceinline__ float dq_bias(const uint8_t* rec, const DLayer& L, int o) {
+  return __uint_as_float(ld_u32u(rec, L.bias_off + 4u * o));
+}
+
+// ---------------------------------------------------------------------------
+// Coordinates: x = f32(f64(c) * (1.0 / (w-1))), last = 1.0, 1-px axis = 0
+// (np.linspace + astype(f32), net.py:146-149).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float grid_coord(int i, int n, double inv) {
+  if (n <= 1) return 0.0f;
+  if (i == n - 1) return 1.0f;
+  return __double2float_rn(double(i) * inv);
+}
+
+struct DecodeArgs {
+  int out_h, out_w, hw;
+  double inv_wm1, inv_hm1;
+  int dtype, layout, aug;
+  int identity;           // mean 0 / std 1: skip the normalise arithmetic
+  float mean[3], stdv[3];
+};
+
+// Source coordinate of output pixel p of image `img` after the crop / flip
+// transform (oracle: augment_coords).  Returns false for padding pixels.
+__device__ __forceinline__ bool pixel_coord(const DecodeArgs& a, const float* __restrict__ aug, int64_t img, int p,
+                                            float& x, float& y) {
+  const int r = p / a.out_w;
+  const int c = p - r * a.out_w;
+  if (a.aug == RINR_AUG_NONE) {
+    x = grid_coord(c, a.out_w, a.inv_wm1);
+    y = grid_coord(r, a.out_h, a.inv_hm1);
+    return true;
+  }
+  const float* q = aug + img * 5;
+  if (a.aug == RINR_AUG_OFFSET) {
+    const int dx = int(q[0]), dy = int(q[1]), flip = int(q[2]), pad = int(q[3]);
+    const int sc = (flip ? a.out_w - 1 - c : c) + dx - pad;
+    const int sr = r + dy - pad;
+    const bool ok = sc >= 0 && sc < a.out_w && sr >= 0 && sr < a.out_h;
+    x = ok ? grid_coord(sc, a.out_w, a.inv_wm1) : 0.0f;
+    y = ok ? grid_coord(sr, a.out_h, a.inv_hm1) : 0.0f;
+    return ok;
+  }
+  const int cx = int(q[4]) ? a.out_w - 1 - c : c;
+  x = __fadd_rn(__fmul_rn(q[2], grid_coord(cx, a.out_w, a.inv_wm1)), q[0]);
+  y = __fadd_rn(__fmul_rn(q[3], grid_coord(r, a.out_h, a.inv_hm1)), q[1]);
+  return true;
+}
+
+// clamp [0,1] (decoder.py:35) -> zero-fill padding -> (v - mean) / std.
+__device__ __forceinline__ float epilogue_value(const DecodeArgs& a, float raw, bool valid, int ch) {
+  float v = fminf(fmaxf(raw, 0.0f), 1.0f);
+  if (!valid) v = 0.0f;
+  if (!a.identity) {
+    // select, not index: a runtime index into the kernel-parameter array would
+    // force a local-memory copy of DecodeArgs
+    const float m = ch == 0 ? a.mean[0] : (ch == 1 ? a.mean[1] : a.mean[2]);
+    const float s = ch == 0 ? a.stdv[0] : (ch == 1 ? a.stdv[1] : a.stdv[2]);
+    v = __fdiv_rn(__fsub_rn(v, m), s);
+  }
+  return v;
+}
+
+// Store one channel value of pixel p of image img.
+__device__ __forceinline__ void store_value(const DecodeArgs& a, void* __restrict__ out, int64_t img, int p, int ch,
+                                            float v) {
+  const int64_t idx = a.layout == RINR_LAYOUT_NCHW ? (img * 3 + ch) * int64_t(a.hw) + p
+                                                   : (img * int64_t(a.hw) + p) * 3 + ch;
+  if (a.dtype == RINR_OUT_F32) {
+    static_cast<float*>(out)[idx] = v;
+  } else if (a.dtype == RINR_OUT_BF16) {
+    static_cast<__nv_bfloat16*>(out)[idx] = __float2bfloat16_rn(v);
+  } else {
+    // floor(v * 255 + 0.5) in f32 (image.py:55, bench.py:67)
+    static_cast<uint8_t*>(out)[idx] = uint8_t(floorf(__fadd_rn(__fmul_rn(v, 255.0f), 0.5f)));
+  }
+}
+
+__device__ __forceinline__ void flag_bad_id(int32_t* status, int64_t n, int64_t i) {
+  if (status) atomicMax(status, int32_t(n - i));
+}
+
+}  // namespace rinr

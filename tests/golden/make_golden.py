@@ -1,0 +1,172 @@
+"""Generate tests/golden/*.npz by running the REAL reference package.
+
+Run in the build container (the reference is not present on GPU boxes):
+
+    PYTHONPATH=/root/reference/pkg/src python tests/golden/make_golden.py
+
+Everything here calls only the reference's public API (rinr.net.init,
+rinr.compressor.prune_l1 / quantize / to_half / dynamic_ratio,
+rinr.archive.serialize / read, rinr.decoder.decode_batch, rinr.net.forward,
+rinr.net.coordinate_grid).  The fixtures pin:
+  * archive bytes written by the reference writer       (our writer, C++ parser)
+  * materialised weights per record (archive.read)      (oracle, GPU dequant)
+  * decoded pixels at several resolutions (decode_batch) (oracle, GPU decode)
+  * forward() on augmented coordinates                   (epilogue checker)
+  * coordinate grids                                     (oracle, GPU coords)
+"""
+
+from __future__ import annotations
+
+import io
+import sys
+from pathlib import Path
+
+import numpy as np
+
+sys.path.insert(0, "/root/reference/pkg/src")
+import rinr  # noqa: E402
+from rinr import archive, compressor, decoder, net  # noqa: E402
+
+OUT = Path(__file__).resolve().parent
+ARCH_A = net.Architecture((2, 15, 15, 3))
+ARCH_C = net.Architecture((2, *([40] * 9), 3))
+
+
+def r1(m):
+    """Last layer w x 20, b = 0.5 (SURVEY §8d 'R1')."""
+    m.layers[-1].w = (m.layers[-1].w * np.float32(20.0)).astype(np.float32)
+    m.layers[-1].b = np.full_like(m.layers[-1].b, 0.5)
+    return m
+
+
+def cifar_ratios(n, seed):
+    rng = np.random.default_rng(seed + 7919)
+    sched = compressor.get_schedule("cifar")
+    return [compressor.dynamic_ratio(sched, float(p)) for p in rng.uniform(28.0, 37.0, n)]
+
+
+def ids(n, start=0):
+    return [f"img{i:08d}" for i in range(start, start + n)]
+
+
+def build_archive(models, rid=None):
+    rid = rid or ids(len(models))
+    recs = [archive.ArchiveRecord(i, m) for i, m in zip(rid, models)]
+    buf = io.BytesIO()
+    archive.write(archive.DatasetArchive(recs), buf)
+    return buf.getvalue()
+
+
+def flat(model):
+    return np.concatenate([np.concatenate([l.w.astype(np.float32).ravel(), l.b.astype(np.float32).ravel()])
+                           for l in model.layers])
+
+
+def store_case(name, data, sizes, n_decode=None):
+    arc = archive.read(io.BytesIO(data))
+    models = [r.model for r in arc.records]
+    P = max(net.param_count(m.arch) for m in models)
+    params = np.zeros((len(models), P), np.float32)
+    for i, m in enumerate(models):
+        f = flat(m)
+        params[i, :f.size] = f
+    out = {"archive": np.frombuffer(data, np.uint8), "params": params}
+    nd = len(models) if n_decode is None else n_decode
+    for (h, w) in sizes:
+        imgs = decoder.decode_batch(models[:nd], h, w)
+        out[f"decode_{h}x{w}"] = np.stack([im.pixels for im in imgs]).astype(np.float32)
+    np.savez_compressed(OUT / f"{name}.npz", **out)
+    print(f"{name}: {len(models)} records, {len(data)} bytes, decodes {sizes}")
+
+
+def main():
+    # C1: fp32 dense arch A, literal init (R0) and R1
+    store_case("c1_r0", build_archive([_src(net.init(ARCH_A, s)) for s in range(8)]), [(32, 32), (17, 23)])
+    store_case("c1_r1", build_archive([_src(r1(net.init(ARCH_A, s))) for s in range(16)]),
+               [(32, 32), (1, 1), (1, 7), (9, 1), (64, 48)])
+    # C2: R1 + per-record cifar ratio prune + affine8
+    ratios = cifar_ratios(32, 0)
+    c2 = [compressor.quantize(compressor.prune_l1(_src(r1(net.init(ARCH_A, s))), r), "affine8")
+          for s, r in zip(range(32), ratios)]
+    store_case("c2", build_archive(c2), [(32, 32), (5, 40)])
+    # C3: arch C, R1, 25% prune, affine8 (224x224 in the bench; smaller here)
+    c3 = [compressor.quantize(compressor.prune_l1(_src(r1(net.init(ARCH_C, s)), 224, 224), 0.25), "affine8")
+          for s in range(3)]
+    store_case("c3", build_archive(c3), [(64, 64), (224, 224)], n_decode=2)
+    # Encoding zoo: every tag/form/const combination the writer can emit,
+    # heterogeneous architectures, odd widths.
+    zoo = []
+    rng = np.random.default_rng(5)
+    for k, dims in enumerate([(2, 15, 15, 3), (2, 1, 3), (2, 8, 3), (2, 5, 7, 3), (2, 32, 32, 32, 3),
+                              (2, 40, 40, 3), (2, 16, 16, 3), (2, 33, 3)]):
+        m = r1(net.init(net.Architecture(dims, omega=float(rng.choice([30.0, 20.0, 1.5]))), 100 + k))
+        for l in m.layers:
+            l.b = rng.normal(0, 0.2, l.b.shape).astype(np.float32)
+        m = _src(m, int(rng.integers(1, 40)), int(rng.integers(1, 40)))
+        kind = k % 4
+        if kind == 0:
+            m = compressor.quantize(compressor.prune_l1(m, 0.3), "affine16")
+        elif kind == 1:
+            m = compressor.to_half(compressor.prune_l1(m, 0.05))
+        elif kind == 2:
+            m = compressor.quantize(compressor.prune_l1(m, 0.1), "affine8")
+        else:
+            m = compressor.prune_l1(m, 0.45) if len(dims) > 4 else compressor.prune_l1(m, 0.12)
+        zoo.append(m)
+    # constant hidden layer (degenerate range -> stored as exact f32)
+    m = _src(r1(net.init(ARCH_A, 999)))
+    m.layers[1].w[:] = np.float32(0.01)
+    zoo.append(compressor.quantize(m, "affine8"))
+    # sparse + constant: a single kept weight
+    m = _src(r1(net.init(ARCH_A, 998)))
+    m.mask[1][:] = False
+    m.mask[1][3, 4] = True
+    m.layers[1].w *= m.mask[1]
+    zoo.append(compressor.quantize(m, "affine8"))
+    store_case("zoo", build_archive(zoo), [(11, 13), (32, 32)])
+
+    # Epilogue checker: forward() on transformed coordinates (AUG_OFFSET/CROP)
+    sys.path.insert(0, str(OUT.parents[1]))
+    from oracle import rinr_oracle as O  # noqa: PLC0415
+    models = c2[:4]
+    aug = {}
+    rng = np.random.default_rng(11)
+    for i, m in enumerate(models):
+        off = [int(rng.integers(0, 9)), int(rng.integers(0, 9)), int(rng.integers(0, 2)), 4, 0]
+        crop = [float(np.float32(rng.uniform(0, 0.5))), float(np.float32(rng.uniform(0, 0.5))),
+                float(np.float32(rng.uniform(0.3, 0.5))), float(np.float32(rng.uniform(0.3, 0.5))),
+                int(rng.integers(0, 2))]
+        for mode, params in ((O.AUG_OFFSET, off), (O.AUG_CROP, crop)):
+            coords, valid = O.augment_coords(32, 32, mode, params)
+            raw = net.forward(m, coords)  # the reference forward at the transformed coordinates
+            aug[f"raw_{mode}_{i}"] = raw.astype(np.float32)
+            aug[f"valid_{mode}_{i}"] = valid
+            aug[f"params_{mode}_{i}"] = np.array(params, np.float32)
+    np.savez_compressed(OUT / "augment.npz", **aug)
+
+    grids = {f"grid_{h}x{w}": net.coordinate_grid(h, w) for h, w in
+             [(1, 1), (1, 5), (6, 1), (3, 4), (32, 32), (7, 224), (224, 224)]}
+    np.savez_compressed(OUT / "grids.npz", **grids)
+
+    # SPEC.md known answers (net.py forward / param_count)
+    kat = {
+        "param_count": np.array([net.param_count(net.Architecture(d)) for d in
+                                 [(2, 1, 3), (2, 15, 15, 3), (2, *([40] * 9), 3)]]),
+    }
+    m = net.InrModel(net.Architecture((2, 1, 3)), [net.LayerWeights(np.array([[1.0, 0.0]], np.float32),
+                                                                     np.zeros(1, np.float32)),
+                                                    net.LayerWeights(np.ones((3, 1), np.float32),
+                                                                     np.zeros(3, np.float32))],
+                     [np.ones((1, 2), bool), np.ones((3, 1), bool)])
+    kat["sin15_forward"] = net.forward(m, np.array([[0.5, 0.0]], np.float32))
+    np.savez_compressed(OUT / "kat.npz", **kat)
+    print("rinr", rinr.__version__, "numpy", np.__version__)
+
+
+def _src(m, h=32, w=32):
+    m.source_h, m.source_w = h, w
+    return m
+
+
+if __name__ == "__main__":
+    main()

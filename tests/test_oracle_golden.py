@@ -1,0 +1,89 @@
+"""Pin the CPU oracle to the real reference: every golden vector produced by
+running /root/reference (tests/golden/make_golden.py) must be reproduced
+bit-for-bit by oracle/rinr_oracle.py."""
+
+import numpy as np
+import pytest
+
+from conftest import STORE_CASES
+from oracle import rinr_oracle as O
+
+
+@pytest.mark.parametrize("case", STORE_CASES)
+def test_materialize_bit_exact(golden, case):
+    g = golden(case)
+    models = O.read_models(g["archive"].tobytes())
+    assert len(models) == g["params"].shape[0]
+    for i, m in enumerate(models):
+        f = O.flat_params(m)
+        np.testing.assert_array_equal(f.view(np.uint32), g["params"][i, :f.size].view(np.uint32))
+
+
+@pytest.mark.parametrize("case", STORE_CASES)
+def test_decode_bit_exact(golden, case):
+    g = golden(case)
+    models = O.read_models(g["archive"].tobytes())
+    for key in g:
+        if not key.startswith("decode_"):
+            continue
+        h, w = map(int, key[len("decode_"):].split("x"))
+        want = g[key]
+        got = np.stack(O.decode_batch(models[:want.shape[0]], h, w))
+        np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+def test_grids(golden):
+    g = golden("grids")
+    for key, want in g.items():
+        h, w = map(int, key[len("grid_"):].split("x"))
+        np.testing.assert_array_equal(O.coordinate_grid(h, w), want)
+        # the closed form the CUDA kernels use: f32(f64(i) * (1/(n-1))), last = 1
+        for n, col in ((w, 0), (h, 1)):
+            if n > 1:
+                closed = (np.arange(n, dtype=np.float64) * (1.0 / (n - 1))).astype(np.float32)
+                closed[-1] = 1.0
+            else:
+                closed = np.zeros(1, np.float32)
+            axis = want[:, col].reshape(h, w)
+            np.testing.assert_array_equal(axis[0, :] if col == 0 else axis[:, 0], closed)
+
+
+def test_augment_checker_matches_reference_forward(golden):
+    g = golden("augment")
+    models = O.read_models(golden("c2")["archive"].tobytes())
+    for key in g:
+        if not key.startswith("raw_"):
+            continue
+        _, mode, i = key.split("_")
+        mode, i = int(mode), int(i)
+        coords, valid = O.augment_coords(32, 32, mode, g[f"params_{mode}_{i}"])
+        np.testing.assert_array_equal(valid, g[f"valid_{mode}_{i}"])
+        np.testing.assert_array_equal(O.forward(models[i], coords).view(np.uint32), g[key].view(np.uint32))
+
+
+def test_known_answers(golden):
+    k = golden("kat")
+    assert list(k["param_count"]) == [9, 333, 13363]
+    np.testing.assert_allclose(k["sin15_forward"], np.sin(np.float32(15.0)), rtol=0, atol=1e-6)
+    m = O.OModel((2, 1, 3), 30.0, [O.OLayer(np.array([[1.0, 0.0]], np.float32), np.zeros(1, np.float32),
+                                            np.ones((1, 2), bool)),
+                                   O.OLayer(np.ones((3, 1), np.float32), np.zeros(3, np.float32),
+                                            np.ones((3, 1), bool))])
+    np.testing.assert_array_equal(O.forward(m, np.array([[0.5, 0.0]], np.float32)), k["sin15_forward"])
+
+
+def test_u8_round_half_away():
+    px = np.array([0.0, 1.0, 0.5 / 255, 1.5 / 255, 0.999, -0.1, 1.2], np.float32)
+    assert list(O.to_u8(px)) == [0, 255, 1, 2, 255, 0, 255]
+
+
+def test_integrity_errors(golden):
+    data = bytearray(golden("c2")["archive"].tobytes())
+    bad = bytearray(data)
+    bad[-1] ^= 0xFF
+    with pytest.raises(O.OracleIntegrityError, match="record 31: CRC mismatch"):
+        O.read_models(bytes(bad))
+    with pytest.raises(O.OracleIntegrityError, match="bad magic"):
+        O.read_models(b"XXXX" + bytes(data[4:]))
+    with pytest.raises(O.OracleIntegrityError, match="truncated"):
+        O.read_models(bytes(data[:-10]))
