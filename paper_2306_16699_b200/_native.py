@@ -67,6 +67,8 @@ def lib() -> C.CDLL:
                                          C.POINTER(C.c_size_t), C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]
     L.rinr_dequantize.argtypes = [vp, vp, i64, vp, i64, vp, vp]
     L.rinr_decode.argtypes = [vp, vp, i64, C.POINTER(DecodeParams), vp, vp, vp, vp]
+    L.rinr_diag_launch.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, C.POINTER(C.c_double)]
+    L.rinr_diag_launch.restype = C.c_int
     for name in EXPORTS:
         if name != "rinr_abi_version" and name not in ("rinr_last_error", "rinr_last_error_record"):
             getattr(L, name).restype = C.c_int
