@@ -1,0 +1,159 @@
+// Uniform-width SIREN decode on mma.sync.m16n8k16 (bf16 operands, f32
+// accumulate), register-resident layer chain.
+//
+// Work unit: one warp evaluates NB blocks of 16 consecutive pixels of one
+// image.  Per block and hidden layer the warp holds the activation tile as
+// bf16 A fragments; the f32 accumulator fragments of n-tiles 2t and 2t+1 are
+// exactly the A fragment of k-tile t of the next layer, so
+// MMA -> scale/bias FFMA -> sine -> bf16 pack -> next MMA stays in registers.
+//
+// Numerics (reference net.py:190-201 is z = a @ w.T + b; a = sin(omega z)):
+//   * omega is folded into weights/biases/scales in the prologue.
+//   * Hidden layers stored as affine8 codes (archive.py:294-301) use the
+//     integer (code - zero_point) as the B operand — exact in bf16 — and apply
+//     f32(omega * scale) after the MMA, so the weights need no hi/lo split.
+//     Other layers use B = omega * w split into bf16 hi + lo.
+//   * X3 (precision FP32): A split into bf16 hi + lo, products
+//     Ah*Bh + Al*Bh (+ Ah*Bl for float B); max-abs vs the CPU oracle ~1e-5.
+//   * BF16: one pass.
+//   * Output layer: bias add + clamp in one saturating FADD (decoder.py:35).
+//     Crop padding enters as NaN coordinates; saturate maps NaN to 0, the
+//     zero fill the epilogue specification asks for.
+#pragma once
+
+#include "device_common.cuh"
+
+namespace rinr {
+
+__device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};\n"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+__device__ __forceinline__ uint32_t bf2_bits(__nv_bfloat162 v) { return *reinterpret_cast<uint32_t*>(&v); }
+
+// (x0, x1) -> packed bf16x2 hi and, for the split, lo = bf16(x - f32(hi)).
+// X3 uses a truncation split: hi = top 16 bits (one byte-permute packs the
+// pair), lo = the exact remainder x - hi rounded to bf16; |x - hi - lo| <= 2^-16 |x|.
+template <bool X3>
+__device__ __forceinline__ void pack_act(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+  if constexpr (X3) {
+    const uint32_t u0 = __float_as_uint(x0), u1 = __float_as_uint(x1);
+    hi = __byte_perm(u0, u1, 0x7632);
+    lo = bf2_bits(__floats2bfloat162_rn(x0 - __uint_as_float(u0 & 0xffff0000u),
+                                        x1 - __uint_as_float(u1 & 0xffff0000u)));
+  } else {
+    hi = bf2_bits(__floats2bfloat162_rn(x0, x1));
+  }
+}
+
+template <bool ACCURATE>
+__device__ __forceinline__ float sine(float x) {
+  if constexpr (ACCURATE) return sinf(x);
+  return __sinf(x);
+}
+
+// Shared-memory image of one record's network, zero padded to the MMA tiles.
+//   fragH[h][t][j][lane] uint4 {b0 hi, b1 hi, b0 lo, b1 lo} of hidden layer h+1
+//   fragO[t][lane]       uint4, last layer (n-tile 0; 3 valid columns)
+//   l0[c]                float4 {omega w[c][0], omega w[c][1], omega b[c], 0}
+//   biasH[h][c]          omega * b;   scaleH[h]: f32(omega*scale) or 1
+//   modeH[h]             1 = integer-code B (affine8), 0 = float B split
+//   biasO[8]
+template <int HID, int NL>
+struct MmaCfg {
+  static constexpr int KP = (HID + 15) / 16 * 16;
+  static constexpr int KT = KP / 16;
+  static constexpr int NT = (HID + 7) / 8;
+  static constexpr int NH = NL - 2;
+  static constexpr int FRAG_H = NH * KT * NT * 32 * 4;  // u32 words
+  static constexpr int FRAG_O = KT * 32 * 4;
+  static constexpr int L0F = KP * 4;
+  static constexpr int BIASH = NH * NT * 8;
+  static constexpr int NHP = (NH + 3) / 4 * 4;
+  static constexpr int NET_WORDS = FRAG_H + FRAG_O + L0F + BIASH + 2 * NHP + 8;
+};
+
+template <int HID, int NL>
+struct NetView {
+  using C = MmaCfg<HID, NL>;
+  uint32_t* fragH;
+  uint32_t* fragO;
+  float* l0;
+  float* biasH;
+  float* scaleH;
+  int* modeH;
+  float* biasO;
+  __device__ explicit NetView(uint32_t* base) {
+    fragH = base;
+    fragO = fragH + C::FRAG_H;
+    l0 = reinterpret_cast<float*>(fragO + C::FRAG_O);
+    biasH = l0 + C::L0F;
+    scaleH = biasH + C::BIASH;
+    modeH = reinterpret_cast<int*>(scaleH + C::NHP);
+    biasO = reinterpret_cast<float*>(modeH + C::NHP);
+  }
+  // B[k][n] entry of a fragment array with NTS n-tiles per k-tile.
+  __device__ __forceinline__ static void put_b(uint32_t* frag, int nts, int k, int n, float hi, float lo) {
+    const int t = k >> 4, kk = k & 15, j = n >> 3, g = n & 7;
+    const int reg = kk >> 3, tq = (kk & 7) >> 1, half = kk & 1;
+    __nv_bfloat16* p = reinterpret_cast<__nv_bfloat16*>(frag + ((t * nts + j) * 32 + g * 4 + tq) * 4);
+    p[reg * 2 + half] = __float2bfloat16_rn(hi);
+    p[(reg + 2) * 2 + half] = __float2bfloat16_rn(lo);
+  }
+  __device__ __forceinline__ static void put_b_split(uint32_t* frag, int nts, int k, int n, float v) {
+    const float h = __bfloat162float(__float2bfloat16_rn(v));
+    put_b(frag, nts, k, n, h, v - h);
+  }
+};
+
+// Per-image coordinate tables (built in the prologue): colx[c], rowy[r] are
+// the source coordinates of output column c / row r after crop / flip; NaN
+// marks padding (AUG_OFFSET outside the source image).
+__device__ __forceinline__ void build_coord_tables(const DecodeArgs& a, const float* __restrict__ aug, int64_t img,
+                                                   float* colx, float* rowy, int tid, int nthr) {
+  const float nan = __int_as_float(0x7fc00000);
+  float q[5] = {0.f, 0.f, 1.f, 1.f, 0.f};
+  if (a.aug != RINR_AUG_NONE) {
+#pragma unroll
+    for (int i = 0; i < 5; ++i) q[i] = aug[img * 5 + i];
+  }
+  for (int i = tid; i < a.out_w + a.out_h; i += nthr) {
+    const bool is_col = i < a.out_w;
+    const int n = is_col ? a.out_w : a.out_h;
+    const double inv = is_col ? a.inv_wm1 : a.inv_hm1;
+    const int k = is_col ? i : i - a.out_w;
+    float v;
+    if (a.aug == RINR_AUG_NONE) {
+      v = grid_coord(k, n, inv);
+    } else if (a.aug == RINR_AUG_OFFSET) {
+      const int s = (is_col ? ((int(q[2]) ? n - 1 - k : k) + int(q[0])) : k + int(q[1])) - int(q[3]);
+      v = (s >= 0 && s < n) ? grid_coord(s, n, inv) : nan;
+    } else {
+      const int kk = (is_col && int(q[4])) ? n - 1 - k : k;
+      v = is_col ? __fadd_rn(__fmul_rn(q[2], grid_coord(kk, n, inv)), q[0])
+                 : __fadd_rn(__fmul_rn(q[3], grid_coord(kk, n, inv)), q[1]);
+    }
+    if (is_col) colx[k] = v;
+    else rowy[k] = v;
+  }
+}
+
+// Affine (code - zero_point) of entry j, or 0 when pruned.
+__device__ __forceinline__ float dq_int(const uint8_t* rec, const DLayer& L, const uint32_t* words,
+                                        const uint32_t* prefix, int j) {
+  bool kept = true;
+  int vi = j;
+  if (L.form != FORM_DENSE) {
+    const uint32_t wd = words[j >> 5];
+    kept = (wd >> (j & 31)) & 1u;
+    if (L.form == FORM_SPARSE) vi = int(prefix[j >> 5] + __popc(wd & ((1u << (j & 31)) - 1u)));
+  }
+  if (!kept) return 0.0f;
+  const int code = int(rec[L.vals_off + vi]);
+  return float(code - L.zp);
+}
+
+}  // namespace rinr

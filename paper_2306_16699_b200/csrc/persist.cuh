@@ -1,0 +1,436 @@
+// Persistent two-phase batched decode (uniform-width SIREN).
+//
+// Grid = one CTA per SM.  The batch is cut into pixel groups (NB blocks of
+// 16 pixels of one image); CTA c owns the contiguous group range
+// [c*T/G, (c+1)*T/G), so every CTA gets the same work to within one group and
+// visits at most ceil(n/G)+1 images.  Those images are processed in chunks of
+// up to `maxi` images (what fits in shared memory), each in two phases:
+//
+//   phase 1 (all warps): fetch the chunk's record metadata, cp.async every
+//     record's bytes from the HBM store into shared memory, build the kept-bit
+//     prefix tables (one warp per sparse layer), then dequantise all entries of
+//     all images in parallel — bit-exact with archive.materialize — straight
+//     into the MMA operand layout (mma_chain.cuh NetView).
+//   phase 2 (all warps): round-robin over the chunk's pixel groups; each warp
+//     runs the register-resident mma.sync layer chain and stores through a
+//     per-warp stage with 16-byte vector stores.
+#pragma once
+
+#include <type_traits>
+
+#include "mma_chain.cuh"
+
+namespace rinr {
+
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
+  const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+struct PersistLayout {
+  int maxi;        // images per chunk
+  int net_words;   // per image
+  int tab_floats;  // per table set: round4(W) + round4(H)
+  int rec_bytes;   // per image record slot (16-B multiple)
+  int pfx_words;   // per image: NL layers x (bit words + prefix)
+  int lay_words;   // per image metadata words (NL + 1 layer offsets, 16-B multiple)
+};
+
+// Per-image operands a warp keeps in registers while decoding that image.
+template <int HID, int NL>
+struct ImgRegs {
+  using C = MmaCfg<HID, NL>;
+  static constexpr int K1 = C::NH == 1 ? C::KT : 1;
+  static constexpr int N1 = C::NH == 1 ? C::NT : 1;
+  float4 w0[C::KT][4];
+  uint4 bo[C::KT];
+  float bias_o0, bias_o1;
+  uint4 bh1[K1][N1];  // hidden layer 1 fragments (only when it is the only hidden layer)
+  float2 bb1[N1];
+  float sc1;
+  bool int1;
+
+  __device__ __forceinline__ void load(const NetView<HID, NL>& net, int lane) {
+    const int tq = lane & 3;
+#pragma unroll
+    for (int t = 0; t < C::KT; ++t)
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        w0[t][q] = reinterpret_cast<const float4*>(net.l0)[16 * t + 2 * tq + (q & 1) + 8 * (q >> 1)];
+#pragma unroll
+    for (int t = 0; t < C::KT; ++t) bo[t] = reinterpret_cast<const uint4*>(net.fragO)[t * 32 + lane];
+    bias_o0 = net.biasO[2 * tq];
+    bias_o1 = net.biasO[2 * tq + 1];
+    if constexpr (C::NH == 1) {
+#pragma unroll
+      for (int t = 0; t < C::KT; ++t)
+#pragma unroll
+        for (int j = 0; j < C::NT; ++j) bh1[t][j] = reinterpret_cast<const uint4*>(net.fragH)[(t * C::NT + j) * 32 + lane];
+#pragma unroll
+      for (int j = 0; j < C::NT; ++j) bb1[j] = *reinterpret_cast<const float2*>(net.biasH + 8 * j + 2 * tq);
+      int1 = net.modeH[0] != 0;
+      sc1 = net.scaleH[0];
+    }
+  }
+};
+
+// One group: NB blocks of 16 pixels of image `img`, pixels [pbase, pbase+16*NB).
+template <int HID, int NL, bool X3, bool ACCURATE, int NB, bool ALIGNED>
+__device__ __forceinline__ void decode_group(const NetView<HID, NL>& net, const ImgRegs<HID, NL>& R,
+                                             const float* colx, const float* rowy, const DecodeArgs& a,
+                                             void* __restrict__ out, int64_t img, int pbase, float invW,
+                                             float* stage, int lane) {
+  using C = MmaCfg<HID, NL>;
+  constexpr int GPX = NB * 16;
+  const int g = lane >> 2, tq = lane & 3;
+  const int W = a.out_w;
+  int rb = int(float(pbase) * invW);
+  int cb = pbase - rb * W;
+  if (cb >= W) { cb -= W; ++rb; }
+  if (cb < 0) { cb += W; --rb; }
+
+  uint32_t ah[NB][C::KT][4], al[NB][C::KT][4];
+#pragma unroll
+  for (int bk = 0; bk < NB; ++bk) {
+    float xr[2], yr[2];
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      if constexpr (ALIGNED) {  // W a multiple of the group: the group lies inside one row
+        xr[h] = colx[cb + 16 * bk + 8 * h + g];
+        yr[h] = rowy[rb];
+      } else {
+        int c = cb + 16 * bk + 8 * h + g, r = rb;
+        while (c >= W) { c -= W; ++r; }
+        const bool inside = pbase + 16 * bk + 8 * h + g < a.hw;
+        xr[h] = colx[inside ? c : 0];
+        yr[h] = rowy[inside ? r : 0];
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < C::KT; ++t) {
+      float s[2][4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const bool pad = 16 * t + 8 * (q >> 1) >= HID;  // whole slot is padding (compile time)
+        const float4 w = R.w0[t][q];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) s[h][q] = pad ? 0.0f : sine<ACCURATE>(fmaf(w.y, yr[h], fmaf(w.x, xr[h], w.z)));
+      }
+      pack_act<X3>(s[0][0], s[0][1], ah[bk][t][0], al[bk][t][0]);
+      pack_act<X3>(s[1][0], s[1][1], ah[bk][t][1], al[bk][t][1]);
+      pack_act<X3>(s[0][2], s[0][3], ah[bk][t][2], al[bk][t][2]);
+      pack_act<X3>(s[1][2], s[1][3], ah[bk][t][3], al[bk][t][3]);
+    }
+  }
+  // ---- hidden layers ---------------------------------------------------------
+#pragma unroll 1
+  for (int hl = 0; hl < C::NH; ++hl) {
+    const uint32_t* fr = net.fragH + hl * C::KT * C::NT * 32 * 4;
+    const bool int_b = C::NH == 1 ? R.int1 : net.modeH[hl] != 0;
+    const float sc = C::NH == 1 ? R.sc1 : net.scaleH[hl];
+    float acc[NB][C::NT][4];
+#pragma unroll
+    for (int bk = 0; bk < NB; ++bk)
+#pragma unroll
+      for (int j = 0; j < C::NT; ++j)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) acc[bk][j][e] = 0.0f;
+    // int_b is warp-uniform: two straight-line MMA sequences instead of a
+    // predicated mma.sync (which would still issue and force warp syncs)
+    auto mma_layer = [&](auto with_lo) {
+#pragma unroll
+      for (int t = 0; t < C::KT; ++t) {
+#pragma unroll
+        for (int j = 0; j < C::NT; ++j) {
+          uint4 bf;
+          if constexpr (C::NH == 1) bf = R.bh1[t][j];
+          else bf = reinterpret_cast<const uint4*>(fr)[(t * C::NT + j) * 32 + lane];
+#pragma unroll
+          for (int bk = 0; bk < NB; ++bk) {
+            mma16816(acc[bk][j], ah[bk][t], bf.x, bf.y);
+            if constexpr (X3) mma16816(acc[bk][j], al[bk][t], bf.x, bf.y);
+            if constexpr (decltype(with_lo)::value) mma16816(acc[bk][j], ah[bk][t], bf.z, bf.w);
+          }
+        }
+      }
+    };
+    if (int_b) mma_layer(std::false_type{});
+    else mma_layer(std::true_type{});
+    float2 bias[C::NT];
+#pragma unroll
+    for (int j = 0; j < C::NT; ++j) {
+      if constexpr (C::NH == 1) bias[j] = R.bb1[j];
+      else bias[j] = *reinterpret_cast<const float2*>(net.biasH + hl * C::NT * 8 + 8 * j + 2 * tq);
+    }
+#pragma unroll
+    for (int bk = 0; bk < NB; ++bk) {
+#pragma unroll
+      for (int t = 0; t < C::KT; ++t) {
+        float s[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const int j = 2 * t + (e >> 2);
+          if (j < C::NT) {
+            const float bias_e = (e & 1) ? bias[j].y : bias[j].x;
+            s[e] = sine<ACCURATE>(fmaf(acc[bk][j][e & 3], sc, bias_e));
+          } else {
+            s[e] = 0.0f;
+          }
+        }
+        pack_act<X3>(s[0], s[1], ah[bk][t][0], al[bk][t][0]);
+        pack_act<X3>(s[2], s[3], ah[bk][t][1], al[bk][t][1]);
+        pack_act<X3>(s[4], s[5], ah[bk][t][2], al[bk][t][2]);
+        pack_act<X3>(s[6], s[7], ah[bk][t][3], al[bk][t][3]);
+      }
+    }
+  }
+  // ---- output layer + epilogue -------------------------------------------------
+  const bool ident = a.identity;
+#pragma unroll
+  for (int bk = 0; bk < NB; ++bk) {
+    float o[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int t = 0; t < C::KT; ++t) {
+      mma16816(o, ah[bk][t], R.bo[t].x, R.bo[t].y);
+      mma16816(o, ah[bk][t], R.bo[t].z, R.bo[t].w);
+      if constexpr (X3) mma16816(o, al[bk][t], R.bo[t].x, R.bo[t].y);
+    }
+    // o[0]=(px g, ch 2tq) o[1]=(g, 2tq+1) o[2]=(g+8, 2tq) o[3]=(g+8, 2tq+1)
+    if (tq < 2) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int odd = e & 1;
+        const int ch = 2 * tq + odd;
+        float v = __saturatef(o[e] + (odd ? R.bias_o1 : R.bias_o0));
+        if (!ident) {
+          const float m = ch == 0 ? a.mean[0] : (ch == 1 ? a.mean[1] : a.mean[2]);
+          const float sd = ch == 0 ? a.stdv[0] : (ch == 1 ? a.stdv[1] : a.stdv[2]);
+          v = __fdiv_rn(__fsub_rn(v, m), sd);
+        }
+        if (ch < 3) stage[ch * GPX + 16 * bk + g + 8 * (e >> 1)] = v;
+      }
+    }
+  }
+  __syncwarp();
+  // ---- coalesced stores -------------------------------------------------------------
+  const bool full = ALIGNED || pbase + GPX <= a.hw;
+  if (full && a.layout == RINR_LAYOUT_NCHW && a.dtype == RINR_OUT_F32 && (a.hw & 3) == 0) {
+    constexpr int V = GPX / 4;
+    if (lane < 3 * V) {
+      const int ch = lane / V, part = lane - ch * V;
+      const float4 v = reinterpret_cast<const float4*>(stage + ch * GPX)[part];
+      reinterpret_cast<float4*>(static_cast<float*>(out) + (img * 3 + ch) * int64_t(a.hw) + pbase)[part] = v;
+    }
+  } else if (full && a.layout == RINR_LAYOUT_NCHW && a.dtype == RINR_OUT_BF16 && (a.hw & 7) == 0) {
+    constexpr int V = GPX / 8;
+    if (lane < 3 * V) {
+      const int ch = lane / V, part = lane - ch * V;
+      const float4 u = reinterpret_cast<const float4*>(stage + ch * GPX)[2 * part];
+      const float4 w = reinterpret_cast<const float4*>(stage + ch * GPX)[2 * part + 1];
+      uint4 pk;
+      pk.x = bf2_bits(__floats2bfloat162_rn(u.x, u.y));
+      pk.y = bf2_bits(__floats2bfloat162_rn(u.z, u.w));
+      pk.z = bf2_bits(__floats2bfloat162_rn(w.x, w.y));
+      pk.w = bf2_bits(__floats2bfloat162_rn(w.z, w.w));
+      reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(out) + (img * 3 + ch) * int64_t(a.hw) + pbase)[part] = pk;
+    }
+  } else if (full && a.layout == RINR_LAYOUT_NHWC && a.dtype == RINR_OUT_F32 && (a.hw & 3) == 0) {
+    constexpr int V = 3 * GPX / 4;
+    if (lane < V) {
+      float e4[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int e = 4 * lane + q, px = e / 3, ch = e - 3 * px;
+        e4[q] = stage[ch * GPX + px];
+      }
+      reinterpret_cast<float4*>(static_cast<float*>(out) + (img * int64_t(a.hw) + pbase) * 3)[lane] =
+          make_float4(e4[0], e4[1], e4[2], e4[3]);
+    }
+  } else {
+    for (int i = lane; i < 3 * GPX; i += 32) {
+      const int ch = i / GPX, q = i - ch * GPX;
+      const int p = pbase + q;
+      if (p < a.hw) store_value(a, out, img, p, ch, stage[i]);
+    }
+  }
+  __syncwarp();
+}
+
+template <int HID, int NL, bool X3, bool ACCURATE, int NW, int NB>
+__global__ void __launch_bounds__(NW * 32, 1)
+    decode_persist(StoreView sv, const int64_t* __restrict__ ids, int64_t n, DecodeArgs a,
+                   const float* __restrict__ aug, void* __restrict__ out, int32_t* status, float omega,
+                   PersistLayout lay) {
+  using C = MmaCfg<HID, NL>;
+  using Net = NetView<HID, NL>;
+  constexpr int NT = NW * 32;
+  constexpr int GPX = NB * 16;
+  // per-image parameter count in the flattened dequant walk (weights + biases)
+  constexpr int P0 = 2 * HID + HID, PH = HID * HID + HID, PO = 3 * HID + 3;
+  constexpr int PALL = P0 + (NL - 2) * PH + PO;
+  constexpr int KW = (HID * HID + 31) / 32 + 1;  // words of one layer's bitset/prefix table
+
+  extern __shared__ __align__(16) uint8_t smem[];
+  const bool shared_tab = a.aug == RINR_AUG_NONE;
+  uint32_t* nets = reinterpret_cast<uint32_t*>(smem);
+  float* tabs = reinterpret_cast<float*>(nets + lay.maxi * lay.net_words);
+  uint8_t* recs = reinterpret_cast<uint8_t*>(tabs + (shared_tab ? 1 : lay.maxi) * lay.tab_floats);
+  uint32_t* pfx = reinterpret_cast<uint32_t*>(recs + size_t(lay.maxi) * lay.rec_bytes);
+  uint32_t* metal = pfx + lay.maxi * lay.pfx_words;                        // [maxi][lay_words] layer offsets
+  int64_t* metaid = reinterpret_cast<int64_t*>(metal + lay.maxi * lay.lay_words);  // [maxi]
+  float* stagebase = reinterpret_cast<float*>(metaid + ((lay.maxi + 1) & ~1));
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int nblk = (a.hw + 15) / 16;
+  const int gpi = (nblk + NB - 1) / NB;  // groups per image
+  const int64_t total = n * gpi;
+  const int64_t G0 = total * blockIdx.x / gridDim.x, G1 = total * (blockIdx.x + 1) / gridDim.x;
+  if (G0 >= G1) return;
+  const int64_t img0 = G0 / gpi;
+  const int nimg = int((G1 - 1) / gpi - img0 + 1);
+  float* stage = stagebase + warp * (3 * GPX);
+  const float invW = 1.0f / float(a.out_w);
+
+  if (shared_tab) build_coord_tables(a, aug, 0, tabs, tabs + ((a.out_w + 3) & ~3), tid, NT);
+
+  for (int c0 = 0; c0 < nimg; c0 += lay.maxi) {
+    const int ni = min(lay.maxi, nimg - c0);
+    const int64_t cimg = img0 + c0;  // first image of the chunk
+    // -------------------------------- phase 1 --------------------------------
+    for (int i = tid; i < ni; i += NT) {
+      const int64_t id = ids[cimg + i];
+      const bool ok = id >= 0 && id < sv.n;
+      if (!ok) flag_bad_id(status, n, cimg + i);
+      metaid[i] = ok ? id : -1;
+    }
+    for (int i = tid; i < ni * lay.net_words / 4; i += NT) reinterpret_cast<uint4*>(nets)[i] = make_uint4(0, 0, 0, 0);
+    if (!shared_tab)
+      for (int i = 0; i < ni; ++i) {
+        float* tab = tabs + i * lay.tab_floats;
+        build_coord_tables(a, aug, cimg + i, tab, tab + ((a.out_w + 3) & ~3), tid, NT);
+      }
+    __syncthreads();
+    for (int q = tid; q < ni * (NL + 1); q += NT) {
+      const int i = q / (NL + 1), l = q - i * (NL + 1);
+      const int64_t id = metaid[i];
+      metal[i * lay.lay_words + l] = id >= 0 ? sv.lay_off[id * sv.lstride + l] : 0u;
+    }
+    __syncthreads();
+    // record bytes -> smem: warp w copies images w, w+NW, ...
+    for (int i = warp; i < ni; i += NW) {
+      const int64_t id = metaid[i];
+      if (id < 0) continue;
+      const uint8_t* src = sv.blob + sv.rec_off[id];
+      const uint32_t bytes = (metal[i * lay.lay_words + NL] + 15u) & ~15u;
+      uint8_t* dst = recs + size_t(i) * lay.rec_bytes;
+      for (uint32_t k = lane; k < bytes / 16; k += 32) cp_async16(dst + 16 * k, src + 16 * k);
+    }
+    cp_async_commit();
+    cp_async_wait_all();
+    __syncthreads();
+    // kept-bit prefix tables: one warp per (image, masked layer)
+    for (int q = warp; q < ni * NL; q += NW) {
+      const int i = q / NL, l = q - i * NL;
+      if (metaid[i] < 0) continue;
+      const uint8_t* rec = recs + size_t(i) * lay.rec_bytes;
+      const uint32_t* lo = metal + i * lay.lay_words;
+      const int fi = l == 0 ? 2 : HID, fo = l == NL - 1 ? 3 : HID;
+      const DLayer L = parse_layer(rec, lo[l], lo[l + 1], fi, fo);
+      if (L.form != FORM_DENSE) {
+        uint32_t* words = pfx + i * lay.pfx_words + l * 2 * KW;
+        build_bit_prefix(rec, L, words, words + KW, lane);
+      }
+    }
+    __syncthreads();
+    // dequantise every parameter of every image of the chunk
+    for (int q = tid; q < ni * PALL; q += NT) {
+      const int i = q / PALL;
+      int e = q - i * PALL;
+      if (metaid[i] < 0) continue;
+      int l, o, k;
+      bool is_bias;
+      if (e < P0) {
+        l = 0;
+        is_bias = e >= 2 * HID;
+        o = is_bias ? e - 2 * HID : e / 2;
+        k = is_bias ? 0 : e - 2 * o;
+      } else if (e < P0 + (NL - 2) * PH) {
+        e -= P0;
+        const int h = e / PH;
+        e -= h * PH;
+        l = 1 + h;
+        is_bias = e >= HID * HID;
+        o = is_bias ? e - HID * HID : e / HID;
+        k = is_bias ? 0 : e - HID * o;
+      } else {
+        e -= P0 + (NL - 2) * PH;
+        l = NL - 1;
+        is_bias = e >= 3 * HID;
+        o = is_bias ? e - 3 * HID : e / HID;
+        k = is_bias ? 0 : e - HID * o;
+      }
+      const uint8_t* rec = recs + size_t(i) * lay.rec_bytes;
+      const uint32_t* lo = metal + i * lay.lay_words;
+      const int fi = l == 0 ? 2 : HID, fo = l == NL - 1 ? 3 : HID;
+      const DLayer L = parse_layer(rec, lo[l], lo[l + 1], fi, fo);
+      const uint32_t* words = pfx + i * lay.pfx_words + l * 2 * KW;
+      const bool hidden = l > 0 && l < NL - 1;
+      const bool int_b = hidden && L.tag == TAG_A8 && !L.cst;
+      Net net(nets + i * lay.net_words);
+      if (is_bias) {
+        const float bb = dq_bias(rec, L, o);
+        if (l == 0) net.l0[o * 4 + 2] = __fmul_rn(omega, bb);
+        else if (hidden) net.biasH[(l - 1) * C::NT * 8 + o] = __fmul_rn(omega, bb);
+        else net.biasO[o] = bb;
+        if (hidden && o == 0) {
+          net.modeH[l - 1] = int_b ? 1 : 0;
+          net.scaleH[l - 1] = int_b ? __double2float_rn(double(omega) * L.scale) : 1.0f;
+        }
+      } else {
+        const int j = o * fi + k;
+        if (l == 0) {
+          net.l0[o * 4 + k] = __fmul_rn(omega, dq_weight(rec, L, words, words + KW, j));
+        } else if (hidden) {
+          uint32_t* fr = net.fragH + (l - 1) * C::KT * C::NT * 32 * 4;
+          if (int_b) Net::put_b(fr, C::NT, k, o, dq_int(rec, L, words, words + KW, j), 0.0f);
+          else Net::put_b_split(fr, C::NT, k, o, __fmul_rn(omega, dq_weight(rec, L, words, words + KW, j)));
+        } else {
+          Net::put_b_split(net.fragO, 1, k, o, dq_weight(rec, L, words, words + KW, j));
+        }
+      }
+    }
+    __syncthreads();
+    // -------------------------------- phase 2 --------------------------------
+    const int64_t cbase = cimg * gpi;
+    const int gs = int((G0 > cbase ? G0 : cbase) - cbase);
+    const int ge = int((G1 < cbase + int64_t(ni) * gpi ? G1 : cbase + int64_t(ni) * gpi) - cbase);
+    const bool aligned = (a.out_w % GPX) == 0;
+    int i = (gs + warp) / gpi, within = gs + warp - i * gpi;
+    int cur = -1;
+    ImgRegs<HID, NL> R;
+    Net net(nets);
+#pragma unroll 1
+    for (int gg = gs + warp; gg < ge; gg += NW) {
+      if (i != cur) {
+        cur = i;
+        net = Net(nets + i * lay.net_words);
+        R.load(net, lane);
+      }
+      const float* colx = shared_tab ? tabs : tabs + i * lay.tab_floats;
+      const float* rowy = colx + ((a.out_w + 3) & ~3);
+      if (aligned)
+        decode_group<HID, NL, X3, ACCURATE, NB, true>(net, R, colx, rowy, a, out, cimg + i, within * GPX, invW,
+                                                      stage, lane);
+      else
+        decode_group<HID, NL, X3, ACCURATE, NB, false>(net, R, colx, rowy, a, out, cimg + i, within * GPX, invW,
+                                                       stage, lane);
+      within += NW;
+      while (within >= gpi) { within -= gpi; ++i; }
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace rinr

@@ -73,8 +73,8 @@ class Store:
 
     def close(self) -> None:
         if getattr(self, "_h", None) is not None and self._h.value:
-            N.check(N.lib().rinr_store_destroy(self._h))
-            self._h = C.c_void_p()
+            h, self._h = self._h, C.c_void_p()  # the handle is freed even if cudaFree reports an error
+            N.check(N.lib().rinr_store_destroy(h))
 
     def __del__(self):
         try:
