@@ -58,6 +58,8 @@ def parse_args(argv=None):
     ap.add_argument("--store-records", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-overlap", action="store_true",
+                    help="do not let a decode's prologue overlap the previous decode (PDL off)")
     ap.add_argument("--cpu-seconds", type=float, default=3.0, help="target wall seconds of the CPU sample")
     return ap.parse_args(argv)
 
@@ -340,11 +342,12 @@ def run_ours(args, W):
         aug = [resized_crop_params(B, generator=torch.Generator().manual_seed(1000 * rank + s)).cuda()
                for s in range(Wu + K)]
         params = st.decode_params(H, Wd, dtype=torch.bfloat16, precision=precision, aug_mode="crop",
-                                  mean=IMAGENET_MEAN, std=IMAGENET_STD)
+                                  mean=IMAGENET_MEAN, std=IMAGENET_STD, overlap_prologue=not args.no_overlap)
         odt = torch.bfloat16
     else:
         aug = [None] * (Wu + K)
-        params = st.decode_params(H, Wd, dtype=torch.float32, precision=precision)
+        params = st.decode_params(H, Wd, dtype=torch.float32, precision=precision,
+                                  overlap_prologue=not args.no_overlap)
         odt = torch.float32
     out = torch.empty((B, 3, H, Wd), dtype=odt, device="cuda")
 
@@ -475,6 +478,7 @@ def run_ours(args, W):
                    "l2": "inputs larger than L2: each step decodes a fresh random batch from a store > 126 MB"
                    if st.info.device_bytes > 126e6 else "store smaller than L2",
                    "parallelism": f"image-sharded x{world}, no decode collective", "timing": "CUDA graph of K launches",
+                   "prologue_overlap": not args.no_overlap,
                    "store_build_s": round(build_s, 2)},
         "roofline": {"bound": "mufu", "achieved": achieved / 1e9, "peak": mufu_peak / 1e9 if mufu_peak else None,
                      "unit": "Gsin/s", "frac": achieved / mufu_peak if mufu_peak else None,

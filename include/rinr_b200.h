@@ -98,7 +98,15 @@ typedef struct {
   int32_t aug_mode;        /* rinr_aug_mode                                  */
   float mean[3];           /* epilogue: (clamp(v) - mean) / std per channel  */
   float std[3];
+  int32_t flags;           /* RINR_FLAG_* bits                               */
 } rinr_decode_params_t;
+
+/* flags: the ids / aug inputs were not written by the kernel that precedes this
+ * decode on the stream (e.g. they came from a host copy, or the previous launch
+ * is another decode), so the prologue (record fetch + dequantisation) may start
+ * while that kernel drains (programmatic dependent launch); outputs are still
+ * written only after it completes. */
+#define RINR_FLAG_OVERLAP_PROLOGUE 1
 
 /* Version of this ABI (RINR_ABI_VERSION). */
 RINR_API int rinr_abi_version(void);

@@ -17,6 +17,7 @@ LAYOUT_NCHW, LAYOUT_NHWC = 0, 1
 PREC_FP32, PREC_BF16, PREC_EXACT = 0, 1, 2
 SIN_MUFU, SIN_ACCURATE = 0, 1
 AUG_NONE, AUG_OFFSET, AUG_CROP = 0, 1, 2
+FLAG_OVERLAP_PROLOGUE = 1
 
 EXPORTS = (
     "rinr_abi_version", "rinr_last_error", "rinr_last_error_record", "rinr_archive_validate",
@@ -40,7 +41,7 @@ class DecodeParams(C.Structure):
     _fields_ = [
         ("out_h", C.c_int32), ("out_w", C.c_int32), ("out_dtype", C.c_int32), ("out_layout", C.c_int32),
         ("precision", C.c_int32), ("sin_mode", C.c_int32), ("aug_mode", C.c_int32),
-        ("mean", C.c_float * 3), ("std", C.c_float * 3),
+        ("mean", C.c_float * 3), ("std", C.c_float * 3), ("flags", C.c_int32),
     ]
 
 

@@ -20,6 +20,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <mutex>
 #include <string>
 #include <unordered_map>
@@ -44,15 +45,19 @@ __global__ void __launch_bounds__(kDqThreads) dequantize_kernel(StoreView sv, co
     if (threadIdx.x == 0) flag_bad_id(status, n, i);
     return;
   }
-  uint8_t* rec = smem;
+  uint8_t* slot = smem;
   const int nwords = (sv.max_width * sv.max_width + 31) / 32 + 1;
-  uint32_t* words = reinterpret_cast<uint32_t*>(smem + sv.max_record_bytes + 16);
+  uint32_t* words = reinterpret_cast<uint32_t*>(smem + sv.max_slot_bytes + 16);
   uint32_t* prefix = words + nwords;
-  const uint32_t* lo = sv.lay_off + id * sv.lstride;
   const uint16_t* dims = sv.arch_dims + int(sv.arch_idx[id]) * kMaxDims;
   const int nl = sv.arch_nd[sv.arch_idx[id]] - 1;
-  copy_record(rec, sv.blob + sv.rec_off[id], (lo[nl] + 15u) & ~15u, threadIdx.x, blockDim.x);
+  uint64_t off;
+  uint32_t bytes;
+  slot_of(sv, id, off, bytes);
+  copy_record(slot, sv.blob + off, bytes, threadIdx.x, blockDim.x);
   __syncthreads();
+  const uint32_t* lo = reinterpret_cast<const uint32_t*>(slot);
+  const uint8_t* rec = slot + sv.hdr_bytes;
   float* dst = out + i * stride;
   for (int l = 0; l < nl; ++l) {
     DLayer L = parse_layer(rec, lo[l], lo[l + 1], dims[l], dims[l + 1]);
@@ -83,9 +88,9 @@ __global__ void __launch_bounds__(kGenThreads) decode_generic(StoreView sv, cons
     return;
   }
   const int tid = threadIdx.x;
-  uint8_t* rec = smem;
+  uint8_t* slot = smem;
   const int nwords = (sv.max_width * sv.max_width + 31) / 32 + 1;
-  uint32_t* words = reinterpret_cast<uint32_t*>(smem + sv.max_record_bytes + 16);
+  uint32_t* words = reinterpret_cast<uint32_t*>(smem + sv.max_slot_bytes + 16);
   uint32_t* prefix = words + nwords;
   float* wts = reinterpret_cast<float*>(prefix + nwords);
   float* act = wts + ((sv.max_params + 3) & ~3);  // [2][max_width][kGenThreads]
@@ -94,9 +99,13 @@ __global__ void __launch_bounds__(kGenThreads) decode_generic(StoreView sv, cons
   const uint16_t* dims = sv.arch_dims + ai * kMaxDims;
   const int nl = sv.arch_nd[ai] - 1;
   const float omega = sv.arch_omega[ai];
-  const uint32_t* lo = sv.lay_off + id * sv.lstride;
-  copy_record(rec, sv.blob + sv.rec_off[id], (lo[nl] + 15u) & ~15u, tid, kGenThreads);
+  uint64_t off;
+  uint32_t bytes;
+  slot_of(sv, id, off, bytes);
+  copy_record(slot, sv.blob + off, bytes, tid, kGenThreads);
   __syncthreads();
+  const uint32_t* lo = reinterpret_cast<const uint32_t*>(slot);
+  const uint8_t* rec = slot + sv.hdr_bytes;
   {
     float* dst = wts;
     for (int l = 0; l < nl; ++l) {
@@ -198,7 +207,7 @@ int rinr_launch_dequantize(const StoreView& sv, const int64_t* d_ids, int64_t n,
   if (d_status && cudaMemsetAsync(d_status, 0, sizeof(int32_t), st) != cudaSuccess)
     return launch_fail("status reset");
   if (n > 0x7FFFFFFF) return set_error(RINR_ERR_INVALID_INPUT, "too many ids in one call");
-  size_t smem = sv.max_record_bytes + 16 + prefix_bytes(sv);
+  size_t smem = sv.max_slot_bytes + 16 + prefix_bytes(sv);
   if (!ensure_smem(dequantize_kernel, smem))
     return launch_fail("dequantize smem attribute");
   dequantize_kernel<<<unsigned(n), kDqThreads, smem, st>>>(sv, d_ids, n, d_out, out_stride, d_status);
@@ -236,25 +245,20 @@ int pick_chunks(int64_t n, int hw, int px_per_cta_min) {
   return chunks;
 }
 
-template <int HID, int NL, bool X3, bool ACC>
-int launch_mma_t(const StoreView& sv, const int64_t* ids, int64_t n, const DecodeArgs& a, const float* aug, void* out,
-                 int32_t* status, cudaStream_t st, float omega) {
-  // 16 warps for the narrow CIFAR net; 8 for the wide nets, whose per-thread
-  // register footprint would not fit 16 warps
-  constexpr int NW = HID <= 16 ? 16 : 8;
-  constexpr int NB = HID <= 16 ? 2 : 1;
+template <int HID, int NL, bool X3, bool ACC, int NW, int NB, class M>
+int launch_persist(const StoreView& sv, const int64_t* ids, int64_t n, const DecodeArgs& a, const float* aug,
+                   void* out, int32_t* status, cudaStream_t st, float omega, int flags) {
   using C = MmaCfg<HID, NL>;
   constexpr int KW = (HID * HID + 31) / 32 + 1;
   PersistLayout lay{};
   lay.net_words = C::NET_WORDS;
   lay.tab_floats = ((a.out_w + 3) & ~3) + ((a.out_h + 3) & ~3);
-  lay.rec_bytes = (sv.max_record_bytes + 16 + 15) & ~15;
+  lay.rec_bytes = (sv.max_slot_bytes + 16 + 15) & ~15;
   lay.pfx_words = (NL * 2 * KW + 3) & ~3;
-  lay.lay_words = (NL + 1 + 3) & ~3;
   const bool shared_tab = a.aug == RINR_AUG_NONE;
   const size_t fixed = size_t(NW) * 3 * NB * 16 * 4 + (shared_tab ? size_t(lay.tab_floats) * 4 : 0) + 64;
-  const size_t per_img = size_t(lay.net_words) * 4 + size_t(lay.rec_bytes) + size_t(lay.pfx_words) * 4 +
-                         size_t(lay.lay_words) * 4 + 8 + (shared_tab ? 0 : size_t(lay.tab_floats) * 4);
+  const size_t per_img = size_t(lay.net_words) * 4 + size_t(lay.rec_bytes) + size_t(lay.pfx_words) * 4 + 8 +
+                         (shared_tab ? 0 : size_t(lay.tab_floats) * 4);
   const size_t budget = 227 * 1024;
   if (fixed + per_img > budget) return set_error(RINR_ERR_UNSUPPORTED, "record or output too large for the decode kernel");
   const int sms = num_sms();
@@ -263,20 +267,59 @@ int launch_mma_t(const StoreView& sv, const int64_t* ids, int64_t n, const Decod
   const int64_t imgs_per_cta = (n + grid - 1) / grid + 1;
   lay.maxi = int(std::min<int64_t>({int64_t((budget - fixed) / per_img), imgs_per_cta, 64}));
   const size_t smem = fixed + size_t(lay.maxi) * per_img;
-  auto kern = decode_persist<HID, NL, X3, ACC, NW, NB>;
+  auto kern = decode_persist<HID, NL, X3, ACC, NW, NB, M>;
   if (!ensure_smem(kern, smem)) return launch_fail("decode_persist smem attribute");
-  kern<<<grid, NW * 32, smem, st>>>(sv, ids, n, a, aug, out, status, omega, lay);
-  if (cudaPeekAtLastError() != cudaSuccess) return launch_fail("decode_persist launch");
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(NW * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const int overlap = (flags & RINR_FLAG_OVERLAP_PROLOGUE) ? 1 : 0;
+  if (cudaLaunchKernelEx(&cfg, kern, sv, ids, n, a, aug, out, status, omega, lay, overlap) != cudaSuccess)
+    return launch_fail("decode_persist launch");
   return RINR_OK;
+}
+
+template <int HID, int NL, bool X3, bool ACC, int NW, int NB>
+int launch_mode(const StoreView& sv, const int64_t* ids, int64_t n, const DecodeArgs& a, const float* aug, void* out,
+                int32_t* status, cudaStream_t st, float omega, int flags) {
+#define RINR_LAUNCH(AL, ST) \
+  launch_persist<HID, NL, X3, ACC, NW, NB, Mode<AL, ST>>(sv, ids, n, a, aug, out, status, st, omega, flags)
+  constexpr int GPX = NB * 16;
+  if constexpr (ACC) {
+    return RINR_LAUNCH(false, 0);  // accurate-sine kernels: one generic store path
+  } else {
+    if (a.out_w % GPX != 0) return RINR_LAUNCH(false, 0);
+    if (a.layout == RINR_LAYOUT_NCHW && a.dtype == RINR_OUT_F32) return RINR_LAUNCH(true, 1);
+    if (a.layout == RINR_LAYOUT_NCHW && a.dtype == RINR_OUT_BF16) return RINR_LAUNCH(true, 2);
+    if (a.layout == RINR_LAYOUT_NHWC && a.dtype == RINR_OUT_F32) return RINR_LAUNCH(true, 3);
+    return RINR_LAUNCH(true, 0);
+  }
+#undef RINR_LAUNCH
+}
+
+template <int HID, int NL, bool X3, bool ACC>
+int launch_mma_t(const StoreView& sv, const int64_t* ids, int64_t n, const DecodeArgs& a, const float* aug, void* out,
+                 int32_t* status, cudaStream_t st, float omega, int flags) {
+  // CTA shape = warps x (16-pixel blocks per warp).  16 x 2 measured best for
+  // the [2,15,15,3] net against (8,4) (8,2) (16,1) (24,1) (32,1); the wide
+  // nets need 8 x 1 to fit their register footprint.
+  if constexpr (HID <= 16) return launch_mode<HID, NL, X3, ACC, 16, 2>(sv, ids, n, a, aug, out, status, st, omega, flags);
+  else return launch_mode<HID, NL, X3, ACC, 8, 1>(sv, ids, n, a, aug, out, status, st, omega, flags);
 }
 
 template <int HID, int NL>
 int launch_mma(const StoreView& sv, const int64_t* ids, int64_t n, const DecodeArgs& a, const float* aug, void* out,
-               int32_t* status, cudaStream_t st, float omega, bool x3, bool acc) {
-  if (x3) return acc ? launch_mma_t<HID, NL, true, true>(sv, ids, n, a, aug, out, status, st, omega)
-                     : launch_mma_t<HID, NL, true, false>(sv, ids, n, a, aug, out, status, st, omega);
-  return acc ? launch_mma_t<HID, NL, false, true>(sv, ids, n, a, aug, out, status, st, omega)
-             : launch_mma_t<HID, NL, false, false>(sv, ids, n, a, aug, out, status, st, omega);
+               int32_t* status, cudaStream_t st, float omega, bool x3, bool acc, int flags) {
+  if (x3) return acc ? launch_mma_t<HID, NL, true, true>(sv, ids, n, a, aug, out, status, st, omega, flags)
+                     : launch_mma_t<HID, NL, true, false>(sv, ids, n, a, aug, out, status, st, omega, flags);
+  return acc ? launch_mma_t<HID, NL, false, true>(sv, ids, n, a, aug, out, status, st, omega, flags)
+             : launch_mma_t<HID, NL, false, false>(sv, ids, n, a, aug, out, status, st, omega, flags);
 }
 
 bool uniform_width(const HostArch& h, int hid, int nl) {
@@ -300,12 +343,12 @@ int rinr_launch_decode(const StoreView& sv, const HostArch* ua, const int64_t* d
   if (ua && p->precision != RINR_PREC_EXACT && a.hw < (1 << 24)) {
     const bool x3 = p->precision == RINR_PREC_FP32;
     const float om = float(ua->omega);
-    if (uniform_width(*ua, 15, 3)) return launch_mma<15, 3>(sv, d_ids, n, a, d_aug, d_out, d_status, st, om, x3, acc);
-    if (uniform_width(*ua, 40, 10)) return launch_mma<40, 10>(sv, d_ids, n, a, d_aug, d_out, d_status, st, om, x3, acc);
-    if (uniform_width(*ua, 32, 10)) return launch_mma<32, 10>(sv, d_ids, n, a, d_aug, d_out, d_status, st, om, x3, acc);
+    if (uniform_width(*ua, 15, 3)) return launch_mma<15, 3>(sv, d_ids, n, a, d_aug, d_out, d_status, st, om, x3, acc, p->flags);
+    if (uniform_width(*ua, 40, 10)) return launch_mma<40, 10>(sv, d_ids, n, a, d_aug, d_out, d_status, st, om, x3, acc, p->flags);
+    if (uniform_width(*ua, 32, 10)) return launch_mma<32, 10>(sv, d_ids, n, a, d_aug, d_out, d_status, st, om, x3, acc, p->flags);
   }
   // Generic fp32 path: weights + per-thread activations in shared memory.
-  const size_t smem = size_t(sv.max_record_bytes) + 16 + prefix_bytes(sv) + size_t((sv.max_params + 3) & ~3) * 4 +
+  const size_t smem = size_t(sv.max_slot_bytes) + 16 + prefix_bytes(sv) + size_t((sv.max_params + 3) & ~3) * 4 +
                       size_t(2) * sv.max_width * kGenThreads * 4;
   if (smem > 227 * 1024)
     return set_error(RINR_ERR_UNSUPPORTED, "architecture too large for the generic decode kernel (" +

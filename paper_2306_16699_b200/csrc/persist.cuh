@@ -28,6 +28,9 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src)
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+// Programmatic dependent launch: wait for the preceding grid / let the next start.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
 struct PersistLayout {
   int maxi;        // images per chunk
@@ -35,7 +38,6 @@ struct PersistLayout {
   int tab_floats;  // per table set: round4(W) + round4(H)
   int rec_bytes;   // per image record slot (16-B multiple)
   int pfx_words;   // per image: NL layers x (bit words + prefix)
-  int lay_words;   // per image metadata words (NL + 1 layer offsets, 16-B multiple)
 };
 
 // Per-image operands a warp keeps in registers while decoding that image.
@@ -51,6 +53,17 @@ struct ImgRegs {
   float2 bb1[N1];
   float sc1;
   bool int1;
+  float mean0, mean1, std0, std1;  // epilogue constants of this lane's channels (2tq, 2tq+1)
+  bool ident;
+
+  __device__ __forceinline__ void set_norm(const DecodeArgs& a, int lane) {
+    const int tq = lane & 3;
+    ident = a.identity != 0;
+    mean0 = tq == 0 ? a.mean[0] : a.mean[2];
+    std0 = tq == 0 ? a.stdv[0] : a.stdv[2];
+    mean1 = a.mean[1];
+    std1 = a.stdv[1];
+  }
 
   __device__ __forceinline__ void load(const NetView<HID, NL>& net, int lane) {
     const int tq = lane & 3;
@@ -76,14 +89,65 @@ struct ImgRegs {
   }
 };
 
+// Phase-2 specialisation, chosen once per launch (warp-uniform):
+//   ALIGNED : out_w is a multiple of the group width, so a group lies inside one
+//             image row and every group is full
+//   STORE   : 1 NCHW f32, 2 NCHW bf16, 3 NHWC f32 (16-byte vector stores,
+//             ALIGNED only), 0 any dtype/layout (scalar stores)
+// Each mode is its own kernel instantiation (one large inlined loop per
+// kernel keeps ptxas from spilling).
+template <bool ALIGNED_, int STORE_>
+struct Mode {
+  static constexpr bool ALIGNED = ALIGNED_;
+  static constexpr int STORE = STORE_;
+};
+
+// Per-lane store addressing, fixed for a launch.
+struct StoreLane {
+  int soff[4];   // stage indices this lane reads
+  int64_t goff;  // element offset of this lane's vector within an image group
+  bool active;
+};
+
+template <int NB, int STORE>
+__device__ __forceinline__ StoreLane make_store_lane(const DecodeArgs& a, int lane) {
+  constexpr int GPX = NB * 16;
+  StoreLane L{};
+  if constexpr (STORE == 1) {  // NCHW f32: lane -> (channel, float4 of the group)
+    constexpr int V = GPX / 4;
+    const int ch = lane / V, part = lane - ch * V;
+    L.active = lane < 3 * V;
+    L.soff[0] = ch * GPX + part * 4;
+    L.goff = int64_t(ch) * a.hw + part * 4;
+  } else if constexpr (STORE == 2) {  // NCHW bf16: lane -> (channel, 8 values)
+    constexpr int V = GPX / 8;
+    const int ch = lane / V, part = lane - ch * V;
+    L.active = lane < 3 * V;
+    L.soff[0] = ch * GPX + part * 8;
+    L.goff = int64_t(ch) * a.hw + part * 8;
+  } else if constexpr (STORE == 3) {  // NHWC f32: lane -> 4 consecutive interleaved values
+    constexpr int V = 3 * GPX / 4;
+    L.active = lane < V;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int e = 4 * lane + q, px = e / 3, ch = e - 3 * px;
+      L.soff[q] = ch * GPX + px;
+    }
+    L.goff = 4 * lane;
+  }
+  return L;
+}
+
 // One group: NB blocks of 16 pixels of image `img`, pixels [pbase, pbase+16*NB).
-template <int HID, int NL, bool X3, bool ACCURATE, int NB, bool ALIGNED>
+// `obase` is the element offset of image img in the output.
+template <int HID, int NL, bool X3, bool ACCURATE, int NB, class M>
 __device__ __forceinline__ void decode_group(const NetView<HID, NL>& net, const ImgRegs<HID, NL>& R,
                                              const float* colx, const float* rowy, const DecodeArgs& a,
-                                             void* __restrict__ out, int64_t img, int pbase, float invW,
-                                             float* stage, int lane) {
+                                             void* __restrict__ out, int64_t img, int64_t obase, int pbase,
+                                             float invW, float* stage, const StoreLane& SL, int lane) {
   using C = MmaCfg<HID, NL>;
   constexpr int GPX = NB * 16;
+  constexpr bool ALIGNED = M::ALIGNED;
   const int g = lane >> 2, tq = lane & 3;
   const int W = a.out_w;
   int rb = int(float(pbase) * invW);
@@ -187,7 +251,6 @@ __device__ __forceinline__ void decode_group(const NetView<HID, NL>& net, const 
     }
   }
   // ---- output layer + epilogue -------------------------------------------------
-  const bool ident = a.identity;
 #pragma unroll
   for (int bk = 0; bk < NB; ++bk) {
     float o[4] = {0.f, 0.f, 0.f, 0.f};
@@ -198,74 +261,91 @@ __device__ __forceinline__ void decode_group(const NetView<HID, NL>& net, const 
       if constexpr (X3) mma16816(o, al[bk][t], R.bo[t].x, R.bo[t].y);
     }
     // o[0]=(px g, ch 2tq) o[1]=(g, 2tq+1) o[2]=(g+8, 2tq) o[3]=(g+8, 2tq+1)
-    if (tq < 2) {
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int odd = e & 1;
-        const int ch = 2 * tq + odd;
-        float v = __saturatef(o[e] + (odd ? R.bias_o1 : R.bias_o0));
-        if (!ident) {
-          const float m = ch == 0 ? a.mean[0] : (ch == 1 ? a.mean[1] : a.mean[2]);
-          const float sd = ch == 0 ? a.stdv[0] : (ch == 1 ? a.stdv[1] : a.stdv[2]);
-          v = __fdiv_rn(__fsub_rn(v, m), sd);
-        }
-        if (ch < 3) stage[ch * GPX + 16 * bk + g + 8 * (e >> 1)] = v;
-      }
+    for (int e = 0; e < 4; ++e) {
+      const int odd = e & 1;
+      const int ch = 2 * tq + odd;
+      float v = __saturatef(o[e] + (odd ? R.bias_o1 : R.bias_o0));
+      if (!R.ident) v = __fdiv_rn(__fsub_rn(v, odd ? R.mean1 : R.mean0), odd ? R.std1 : R.std0);
+      if (ch < 3) stage[ch * GPX + 16 * bk + g + 8 * (e >> 1)] = v;
     }
   }
   __syncwarp();
   // ---- coalesced stores -------------------------------------------------------------
-  const bool full = ALIGNED || pbase + GPX <= a.hw;
-  if (full && a.layout == RINR_LAYOUT_NCHW && a.dtype == RINR_OUT_F32 && (a.hw & 3) == 0) {
-    constexpr int V = GPX / 4;
-    if (lane < 3 * V) {
-      const int ch = lane / V, part = lane - ch * V;
-      const float4 v = reinterpret_cast<const float4*>(stage + ch * GPX)[part];
-      reinterpret_cast<float4*>(static_cast<float*>(out) + (img * 3 + ch) * int64_t(a.hw) + pbase)[part] = v;
+  if constexpr (M::STORE == 1) {
+    if (SL.active) {
+      const float4 v = *reinterpret_cast<const float4*>(stage + SL.soff[0]);
+      *reinterpret_cast<float4*>(static_cast<float*>(out) + obase + SL.goff + pbase) = v;
     }
-  } else if (full && a.layout == RINR_LAYOUT_NCHW && a.dtype == RINR_OUT_BF16 && (a.hw & 7) == 0) {
-    constexpr int V = GPX / 8;
-    if (lane < 3 * V) {
-      const int ch = lane / V, part = lane - ch * V;
-      const float4 u = reinterpret_cast<const float4*>(stage + ch * GPX)[2 * part];
-      const float4 w = reinterpret_cast<const float4*>(stage + ch * GPX)[2 * part + 1];
+  } else if constexpr (M::STORE == 2) {
+    if (SL.active) {
+      const float4 u = *reinterpret_cast<const float4*>(stage + SL.soff[0]);
+      const float4 w = *reinterpret_cast<const float4*>(stage + SL.soff[0] + 4);
       uint4 pk;
       pk.x = bf2_bits(__floats2bfloat162_rn(u.x, u.y));
       pk.y = bf2_bits(__floats2bfloat162_rn(u.z, u.w));
       pk.z = bf2_bits(__floats2bfloat162_rn(w.x, w.y));
       pk.w = bf2_bits(__floats2bfloat162_rn(w.z, w.w));
-      reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(out) + (img * 3 + ch) * int64_t(a.hw) + pbase)[part] = pk;
+      *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(out) + obase + SL.goff + pbase) = pk;
     }
-  } else if (full && a.layout == RINR_LAYOUT_NHWC && a.dtype == RINR_OUT_F32 && (a.hw & 3) == 0) {
-    constexpr int V = 3 * GPX / 4;
-    if (lane < V) {
-      float e4[4];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int e = 4 * lane + q, px = e / 3, ch = e - 3 * px;
-        e4[q] = stage[ch * GPX + px];
-      }
-      reinterpret_cast<float4*>(static_cast<float*>(out) + (img * int64_t(a.hw) + pbase) * 3)[lane] =
-          make_float4(e4[0], e4[1], e4[2], e4[3]);
-    }
+  } else if constexpr (M::STORE == 3) {
+    if (SL.active)
+      *reinterpret_cast<float4*>(static_cast<float*>(out) + obase + SL.goff + int64_t(pbase) * 3) =
+          make_float4(stage[SL.soff[0]], stage[SL.soff[1]], stage[SL.soff[2]], stage[SL.soff[3]]);
   } else {
     for (int i = lane; i < 3 * GPX; i += 32) {
       const int ch = i / GPX, q = i - ch * GPX;
       const int p = pbase + q;
-      if (p < a.hw) store_value(a, out, img, p, ch, stage[i]);
+      if (ALIGNED || p < a.hw) store_value(a, out, img, p, ch, stage[i]);
     }
   }
   __syncwarp();
 }
 
-template <int HID, int NL, bool X3, bool ACCURATE, int NW, int NB>
+// Phase 2 of one chunk: the warp's round-robin share of groups [gs, ge)
+// (group indices relative to the chunk's first image cimg).
+template <int HID, int NL, bool X3, bool ACCURATE, int NW, int NB, class M>
+__device__ __forceinline__ void phase2_loop(const uint32_t* nets, const float* tabs, const PersistLayout& lay,
+                                            bool shared_tab, const DecodeArgs& a, void* __restrict__ out,
+                                            int64_t cimg, int gs, int ge, int gpi, float invW, float* stage,
+                                            int warp, int lane) {
+  using Net = NetView<HID, NL>;
+  constexpr int GPX = NB * 16;
+  const StoreLane SL = make_store_lane<NB, M::STORE>(a, lane);
+  int i = (gs + warp) / gpi, within = gs + warp - i * gpi;
+  int cur = -1;
+  ImgRegs<HID, NL> R;
+  R.set_norm(a, lane);
+  Net net(const_cast<uint32_t*>(nets));
+  int64_t obase = 0;
+#pragma unroll 1
+  for (int gg = gs + warp; gg < ge; gg += NW) {
+    if (i != cur) {
+      cur = i;
+      net = Net(const_cast<uint32_t*>(nets) + i * lay.net_words);
+      R.load(net, lane);
+      obase = (cimg + i) * 3 * int64_t(a.hw);
+    }
+    const float* colx = shared_tab ? tabs : tabs + i * lay.tab_floats;
+    const float* rowy = colx + ((a.out_w + 3) & ~3);
+    decode_group<HID, NL, X3, ACCURATE, NB, M>(net, R, colx, rowy, a, out, cimg + i, obase, within * GPX, invW, stage,
+                                               SL, lane);
+    within += NW;
+    while (within >= gpi) { within -= gpi; ++i; }
+  }
+}
+
+template <int HID, int NL, bool X3, bool ACCURATE, int NW, int NB, class M>
 __global__ void __launch_bounds__(NW * 32, 1)
     decode_persist(StoreView sv, const int64_t* __restrict__ ids, int64_t n, DecodeArgs a,
                    const float* __restrict__ aug, void* __restrict__ out, int32_t* status, float omega,
-                   PersistLayout lay) {
+                   PersistLayout lay, int overlap) {
   using C = MmaCfg<HID, NL>;
   using Net = NetView<HID, NL>;
   constexpr int NT = NW * 32;
+  // Without the overlap promise the inputs may come from the preceding kernel:
+  // wait for it before reading anything.
+  if (!overlap) pdl_wait();
   constexpr int GPX = NB * 16;
   // per-image parameter count in the flattened dequant walk (weights + biases)
   constexpr int P0 = 2 * HID + HID, PH = HID * HID + HID, PO = 3 * HID + 3;
@@ -278,8 +358,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
   float* tabs = reinterpret_cast<float*>(nets + lay.maxi * lay.net_words);
   uint8_t* recs = reinterpret_cast<uint8_t*>(tabs + (shared_tab ? 1 : lay.maxi) * lay.tab_floats);
   uint32_t* pfx = reinterpret_cast<uint32_t*>(recs + size_t(lay.maxi) * lay.rec_bytes);
-  uint32_t* metal = pfx + lay.maxi * lay.pfx_words;                        // [maxi][lay_words] layer offsets
-  int64_t* metaid = reinterpret_cast<int64_t*>(metal + lay.maxi * lay.lay_words);  // [maxi]
+  int64_t* metaid = reinterpret_cast<int64_t*>(pfx + lay.maxi * lay.pfx_words);  // [maxi]
   float* stagebase = reinterpret_cast<float*>(metaid + ((lay.maxi + 1) & ~1));
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -299,43 +378,38 @@ __global__ void __launch_bounds__(NW * 32, 1)
     const int ni = min(lay.maxi, nimg - c0);
     const int64_t cimg = img0 + c0;  // first image of the chunk
     // -------------------------------- phase 1 --------------------------------
-    for (int i = tid; i < ni; i += NT) {
+    // Slot copies: warp w fetches the ids of images w, w+NW, ... and streams
+    // their slots into shared memory (one dependent load: the id).
+    for (int i = warp; i < ni; i += NW) {
       const int64_t id = ids[cimg + i];
       const bool ok = id >= 0 && id < sv.n;
-      if (!ok) flag_bad_id(status, n, cimg + i);
-      metaid[i] = ok ? id : -1;
+      if (lane == 0) {
+        if (!ok) flag_bad_id(status, n, cimg + i);
+        metaid[i] = ok ? id : -1;
+      }
+      if (!ok) continue;
+      uint64_t off;
+      uint32_t bytes;
+      slot_of(sv, id, off, bytes);
+      const uint8_t* src = sv.blob + off;
+      uint8_t* dst = recs + size_t(i) * lay.rec_bytes;
+      for (uint32_t k = lane; k < bytes / 16; k += 32) cp_async16(dst + 16 * k, src + 16 * k);
     }
+    cp_async_commit();
     for (int i = tid; i < ni * lay.net_words / 4; i += NT) reinterpret_cast<uint4*>(nets)[i] = make_uint4(0, 0, 0, 0);
     if (!shared_tab)
       for (int i = 0; i < ni; ++i) {
         float* tab = tabs + i * lay.tab_floats;
         build_coord_tables(a, aug, cimg + i, tab, tab + ((a.out_w + 3) & ~3), tid, NT);
       }
-    __syncthreads();
-    for (int q = tid; q < ni * (NL + 1); q += NT) {
-      const int i = q / (NL + 1), l = q - i * (NL + 1);
-      const int64_t id = metaid[i];
-      metal[i * lay.lay_words + l] = id >= 0 ? sv.lay_off[id * sv.lstride + l] : 0u;
-    }
-    __syncthreads();
-    // record bytes -> smem: warp w copies images w, w+NW, ...
-    for (int i = warp; i < ni; i += NW) {
-      const int64_t id = metaid[i];
-      if (id < 0) continue;
-      const uint8_t* src = sv.blob + sv.rec_off[id];
-      const uint32_t bytes = (metal[i * lay.lay_words + NL] + 15u) & ~15u;
-      uint8_t* dst = recs + size_t(i) * lay.rec_bytes;
-      for (uint32_t k = lane; k < bytes / 16; k += 32) cp_async16(dst + 16 * k, src + 16 * k);
-    }
-    cp_async_commit();
     cp_async_wait_all();
     __syncthreads();
     // kept-bit prefix tables: one warp per (image, masked layer)
     for (int q = warp; q < ni * NL; q += NW) {
       const int i = q / NL, l = q - i * NL;
       if (metaid[i] < 0) continue;
-      const uint8_t* rec = recs + size_t(i) * lay.rec_bytes;
-      const uint32_t* lo = metal + i * lay.lay_words;
+      const uint32_t* lo = reinterpret_cast<const uint32_t*>(recs + size_t(i) * lay.rec_bytes);
+      const uint8_t* rec = recs + size_t(i) * lay.rec_bytes + sv.hdr_bytes;
       const int fi = l == 0 ? 2 : HID, fo = l == NL - 1 ? 3 : HID;
       const DLayer L = parse_layer(rec, lo[l], lo[l + 1], fi, fo);
       if (L.form != FORM_DENSE) {
@@ -371,8 +445,8 @@ __global__ void __launch_bounds__(NW * 32, 1)
         o = is_bias ? e - 3 * HID : e / HID;
         k = is_bias ? 0 : e - HID * o;
       }
-      const uint8_t* rec = recs + size_t(i) * lay.rec_bytes;
-      const uint32_t* lo = metal + i * lay.lay_words;
+      const uint32_t* lo = reinterpret_cast<const uint32_t*>(recs + size_t(i) * lay.rec_bytes);
+      const uint8_t* rec = recs + size_t(i) * lay.rec_bytes + sv.hdr_bytes;
       const int fi = l == 0 ? 2 : HID, fo = l == NL - 1 ? 3 : HID;
       const DLayer L = parse_layer(rec, lo[l], lo[l + 1], fi, fo);
       const uint32_t* words = pfx + i * lay.pfx_words + l * 2 * KW;
@@ -403,32 +477,15 @@ __global__ void __launch_bounds__(NW * 32, 1)
     }
     __syncthreads();
     // -------------------------------- phase 2 --------------------------------
+    if (c0 == 0) {
+      if (overlap) pdl_wait();  // outputs may still be read/written by the preceding grid
+      pdl_trigger();            // every CTA is resident: the next launch may start its prologue
+    }
     const int64_t cbase = cimg * gpi;
     const int gs = int((G0 > cbase ? G0 : cbase) - cbase);
     const int ge = int((G1 < cbase + int64_t(ni) * gpi ? G1 : cbase + int64_t(ni) * gpi) - cbase);
-    const bool aligned = (a.out_w % GPX) == 0;
-    int i = (gs + warp) / gpi, within = gs + warp - i * gpi;
-    int cur = -1;
-    ImgRegs<HID, NL> R;
-    Net net(nets);
-#pragma unroll 1
-    for (int gg = gs + warp; gg < ge; gg += NW) {
-      if (i != cur) {
-        cur = i;
-        net = Net(nets + i * lay.net_words);
-        R.load(net, lane);
-      }
-      const float* colx = shared_tab ? tabs : tabs + i * lay.tab_floats;
-      const float* rowy = colx + ((a.out_w + 3) & ~3);
-      if (aligned)
-        decode_group<HID, NL, X3, ACCURATE, NB, true>(net, R, colx, rowy, a, out, cimg + i, within * GPX, invW,
-                                                      stage, lane);
-      else
-        decode_group<HID, NL, X3, ACCURATE, NB, false>(net, R, colx, rowy, a, out, cimg + i, within * GPX, invW,
-                                                       stage, lane);
-      within += NW;
-      while (within >= gpi) { within -= gpi; ++i; }
-    }
+    phase2_loop<HID, NL, X3, ACCURATE, NW, NB, M>(nets, tabs, lay, shared_tab, a, out, cimg, gs, ge, gpi, invW, stage,
+                                                  warp, lane);
     __syncthreads();
   }
 }

@@ -20,14 +20,20 @@ constexpr int kBlobTailPad = 64;      // over-read slack after the last record
 
 // Device-side view of an immutable store.  Passed by value to kernels.
 //
-// HBM layout (one allocation each):
-//   blob     : record bodies (id .. last bias; CRC stripped), each starting at
-//              a 16-B aligned offset so a whole record moves with 16-B vector
-//              loads / one bulk copy; followed by kBlobTailPad zero bytes.
-//   rec_off  : u64 [n]          byte offset of record k in blob
-//   lay_off  : u32 [n * lstride] offset (from record start) of each layer's
-//              tag byte; entry [n_layers] = end of the body.  The bias of layer
-//              l therefore sits at lay_off[l+1] - 4*out_l.
+// HBM layout (one allocation):
+//   blob     : one 16-B aligned slot per record:
+//                [u32 layer offsets x lstride, zero padded to hdr_bytes]
+//                [record body (id .. last bias; CRC stripped), padded to 16 B]
+//              Layer offset l is the position of layer l's tag byte relative
+//              to the body start; entry [n_layers] is the end of the body, so
+//              the bias of layer l sits at off[l+1] - 4*out_l.  A whole slot
+//              moves with 16-B vector loads / cp.async.  When record sizes are
+//              close (always, for a homogeneous dataset) every slot has the
+//              same size `slot_stride` and slot k starts at k * slot_stride,
+//              so a kernel reaches a record with a single dependent load (the
+//              id); otherwise slot_stride = 0 and rec_off[k]..rec_off[k+1]
+//              bound slot k.  kBlobTailPad zero bytes follow the last slot.
+//   rec_off  : u64 [n + 1]      slot boundaries
 //   arch_idx : u16 [n]          index into the architecture table
 //   arch_dims: u16 [n_arch * kMaxDims], arch_nd: i32 [n_arch],
 //   arch_omega: f32 [n_arch]    f32(omega) as the reference's forward uses it
@@ -35,18 +41,32 @@ constexpr int kBlobTailPad = 64;      // over-read slack after the last record
 struct StoreView {
   const uint8_t* blob;
   const uint64_t* rec_off;
-  const uint32_t* lay_off;
   const uint16_t* arch_idx;
   const uint16_t* arch_dims;
   const int32_t* arch_nd;
   const float* arch_omega;
   int64_t n;
-  int32_t lstride;
+  int32_t lstride;          // layer-offset entries per slot header (max layers + 1)
+  int32_t hdr_bytes;        // slot header size (16-B multiple)
+  int64_t slot_stride;      // fixed slot size, or 0 for variable slots
   int32_t n_arch;
-  int32_t max_record_bytes;   // rounded up to 16
+  int32_t max_slot_bytes;   // largest slot (16-B multiple)
   int32_t max_params;
   int32_t max_width;
 };
+
+// Slot of record `id`: start and size in bytes.
+#ifdef __CUDACC__
+__device__ __forceinline__ void slot_of(const StoreView& sv, int64_t id, uint64_t& off, uint32_t& bytes) {
+  if (sv.slot_stride) {
+    off = uint64_t(id) * uint64_t(sv.slot_stride);
+    bytes = uint32_t(sv.slot_stride);
+  } else {
+    off = sv.rec_off[id];
+    bytes = uint32_t(sv.rec_off[id + 1] - off);
+  }
+}
+#endif
 
 struct HostArch {
   int nd;

@@ -296,8 +296,6 @@ int rinr_store_create(const void* bytes, size_t len, int device, uint32_t shard_
 
   // Architecture table + per-record metadata.
   int lmax = 1, maxw = 1;
-  std::vector<uint64_t> rec_off(n);
-  size_t blob = 0;
   st->ids.resize(n);
   st->src_h.resize(n);
   st->src_w.resize(n);
@@ -326,8 +324,6 @@ int rinr_store_create(const void* bytes, size_t len, int device, uint32_t shard_
       maxw = std::max(maxw, int(r.arch.dims[l + 1]));
     }
     st->max_params = std::max(st->max_params, params);
-    rec_off[i] = blob;
-    blob += (r.body_len + kRecordAlign - 1) / kRecordAlign * kRecordAlign;
     st->max_record_bytes = std::max<int64_t>(st->max_record_bytes, r.body_len);
     st->ids[i] = std::move(r.id);
     st->src_h[i] = r.source_h;
@@ -335,13 +331,28 @@ int rinr_store_create(const void* bytes, size_t len, int device, uint32_t shard_
     if (i > 0 && (r.source_h != st->src_h[0] || r.source_w != st->src_w[0])) st->uniform_source = false;
   }
   st->uniform_arch = st->archs.size() <= 1;
-  blob += kBlobTailPad;
   const int lstride = lmax + 1;
+  const uint32_t hdr = uint32_t((4 * lstride + kRecordAlign - 1) / kRecordAlign * kRecordAlign);
+  // Slots: fixed stride when sizes are within 15% of the largest (saves the
+  // offset lookup on the kernel's critical path), variable otherwise.
+  std::vector<uint64_t> rec_off(n + 1, 0);
+  uint64_t sum = 0, max_slot = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    const uint64_t sl = hdr + (pa.recs[i].body_len + kRecordAlign - 1) / kRecordAlign * kRecordAlign;
+    sum += sl;
+    max_slot = std::max(max_slot, sl);
+  }
+  const bool fixed = n > 0 && double(max_slot) * double(n) <= 1.15 * double(sum);
+  for (int64_t i = 0; i < n; ++i) {
+    const uint64_t sl = fixed ? max_slot : hdr + (pa.recs[i].body_len + kRecordAlign - 1) / kRecordAlign * kRecordAlign;
+    rec_off[i + 1] = rec_off[i] + sl;
+  }
+  const size_t blob = rec_off[n] + kBlobTailPad;
 
   // Host staging of every device array, then one upload.
   auto al = [](size_t x) { return (x + 255) / 256 * 256; };
-  size_t o_blob = 0, o_rec = al(blob), o_lay = o_rec + al(8 * std::max<int64_t>(n, 1));
-  size_t o_aidx = o_lay + al(4 * std::max<int64_t>(n, 1) * lstride);
+  size_t o_blob = 0, o_rec = al(blob);
+  size_t o_aidx = o_rec + al(8 * size_t(n + 1));
   size_t na = std::max<size_t>(st->archs.size(), 1);
   size_t o_adims = o_aidx + al(2 * std::max<int64_t>(n, 1));
   size_t o_and = o_adims + al(2 * na * kMaxDims);
@@ -356,11 +367,11 @@ int rinr_store_create(const void* bytes, size_t len, int device, uint32_t shard_
   const uint8_t* src = static_cast<const uint8_t*>(bytes);
   for (int64_t i = 0; i < n; ++i) {
     const ParsedRecord& r = pa.recs[i];
-    std::memcpy(host.data() + o_blob + rec_off[i], src + r.body_off, r.body_len);
-    uint32_t* lo = reinterpret_cast<uint32_t*>(host.data() + o_lay) + size_t(i) * lstride;
-    for (size_t l = 0; l < r.lay_off.size(); ++l) lo[l] = r.lay_off[l];
+    uint8_t* slot = host.data() + o_blob + rec_off[i];
+    for (size_t l = 0; l < r.lay_off.size(); ++l) std::memcpy(slot + 4 * l, &r.lay_off[l], 4);
+    std::memcpy(slot + hdr, src + r.body_off, r.body_len);
   }
-  std::memcpy(host.data() + o_rec, rec_off.data(), 8 * n);
+  std::memcpy(host.data() + o_rec, rec_off.data(), 8 * size_t(n + 1));
   std::memcpy(host.data() + o_aidx, st->arch_of.data(), 2 * n);
   for (size_t a = 0; a < st->archs.size(); ++a) {
     const HostArch& h = st->archs[a];
@@ -389,15 +400,16 @@ int rinr_store_create(const void* bytes, size_t len, int device, uint32_t shard_
   StoreView& v = st->view;
   v.blob = d + o_blob;
   v.rec_off = reinterpret_cast<const uint64_t*>(d + o_rec);
-  v.lay_off = reinterpret_cast<const uint32_t*>(d + o_lay);
   v.arch_idx = reinterpret_cast<const uint16_t*>(d + o_aidx);
   v.arch_dims = reinterpret_cast<const uint16_t*>(d + o_adims);
   v.arch_nd = reinterpret_cast<const int32_t*>(d + o_and);
   v.arch_omega = reinterpret_cast<const float*>(d + o_aom);
   v.n = n;
   v.lstride = lstride;
+  v.hdr_bytes = int32_t(hdr);
+  v.slot_stride = fixed ? int64_t(max_slot) : 0;
   v.n_arch = int32_t(st->archs.size());
-  v.max_record_bytes = int32_t((st->max_record_bytes + 15) / 16 * 16);
+  v.max_slot_bytes = int32_t(max_slot);
   v.max_params = int32_t(st->max_params);
   v.max_width = maxw;
   *out = st.release();

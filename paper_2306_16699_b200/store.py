@@ -115,7 +115,10 @@ class Store:
         return out
 
     def decode_params(self, out_h, out_w, dtype=torch.float32, layout="nchw", precision="fp32", sin="mufu",
-                      aug_mode=None, mean=None, std=None) -> N.DecodeParams:
+                      aug_mode=None, mean=None, std=None, overlap_prologue: bool = False) -> N.DecodeParams:
+        """``overlap_prologue``: promise that ids/aug were not written by the
+        kernel launched just before this decode on the stream, letting the
+        record fetch + dequantisation overlap that kernel's tail (PDL)."""
         if out_h is None or out_w is None:
             if not self.info.uniform_source:
                 raise InvalidInputError("records differ in source size; pass out_h and out_w")
@@ -132,6 +135,7 @@ class Store:
         p.aug_mode = _AUG[aug_mode]
         p.mean[:] = list(mean) if mean is not None else [0.0, 0.0, 0.0]
         p.std[:] = list(std) if std is not None else [1.0, 1.0, 1.0]
+        p.flags = N.FLAG_OVERLAP_PROLOGUE if overlap_prologue else 0
         return p
 
     def decode(self, ids, out_h=None, out_w=None, *, out=None, dtype=torch.float32, layout="nchw",

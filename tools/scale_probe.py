@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--records", type=int, default=65536)
     ap.add_argument("--precision", default=None)
     ap.add_argument("--reps", type=int, default=50)
+    ap.add_argument("--overlap", action="store_true")
     a = ap.parse_args()
     W = bench.workload(a.config)
     st = Store(bench.store_bytes(a.config, a.records, seed=0))
@@ -34,11 +35,11 @@ def main():
         if a.config == "c3":
             aug = resized_crop_params(B, generator=torch.Generator().manual_seed(0)).cuda()
             p = st.decode_params(H, Wd, dtype=torch.bfloat16, precision=prec, aug_mode="crop", mean=IMAGENET_MEAN,
-                                 std=IMAGENET_STD)
+                                 std=IMAGENET_STD, overlap_prologue=a.overlap)
             out = torch.empty((B, 3, H, Wd), dtype=torch.bfloat16, device="cuda")
         else:
             aug = None
-            p = st.decode_params(H, Wd, precision=prec)
+            p = st.decode_params(H, Wd, precision=prec, overlap_prologue=a.overlap)
             out = torch.empty((B, 3, H, Wd), device="cuda")
         for k in range(3):
             st.decode(ids[k], out=out, aug=aug, params=p, check=False)
@@ -55,7 +56,7 @@ def main():
         e1.record()
         torch.cuda.synchronize()
         us = e0.elapsed_time(e1) * 1e3 / a.reps
-        print(f"{a.config} {prec} batch {B:6d}: {us:9.2f} us/launch  {B / us:8.3f} Mimg/s  {us / B * 1e3:8.3f} ns/img",
+        print(f"{a.config} {prec} ov={int(a.overlap)} batch {B:6d}: {us:9.2f} us/launch  {B / us:8.3f} Mimg/s  {us / B * 1e3:8.3f} ns/img",
               flush=True)
 
 
