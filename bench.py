@@ -60,7 +60,6 @@ def parse_args(argv=None):
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-overlap", action="store_true",
                     help="do not let a decode's prologue overlap the previous decode (PDL off)")
-    ap.add_argument("--cpu-seconds", type=float, default=3.0, help="target wall seconds of the CPU sample")
     return ap.parse_args(argv)
 
 
@@ -159,7 +158,7 @@ def crop_params_np(n: int, seed: int) -> np.ndarray:
     return resized_crop_params(n, generator=torch.Generator().manual_seed(seed)).numpy()
 
 
-def cpu_measure(cfg: str, W: dict, seconds: float, steps: int = None):
+def cpu_measure(cfg: str, W: dict, steps: int = None):
     """Time the reference algorithm on the host cores.  Returns
     (images/s, sample description, cores, per-step times)."""
     cores = host_cores()
@@ -175,8 +174,8 @@ def cpu_measure(cfg: str, W: dict, seconds: float, steps: int = None):
         t = pool.run(ids, aug)
         per_img = t / len(ids)
         times = []
-        if steps is None:  # bounded sample sized to ~`seconds` of wall time
-            n = int(max(len(ids), min(B * 64, seconds / max(per_img, 1e-9))))
+        if steps is None:  # bounded sample: ~10-30 s of CPU work across the cores
+            n = min(262144, cores * 8192) if cfg != "c3" else cores * 8
             ids = rng.integers(0, n_rec, n)
             aug = crop_params_np(n, 1) if cfg == "c3" else None
             t = pool.run(ids, aug)
@@ -201,7 +200,7 @@ def run_reference(args, W):
     if rank != 0:
         return 0
     total = args.warmup + args.steps
-    _, sample, cores, times = cpu_measure(args.config, W, 0, steps=total)
+    _, sample, cores, times = cpu_measure(args.config, W, steps=total)
     t = sum(times[args.warmup:])
     per_step = W["batch"] if args.config != "c3" else max(cores, 16)
     value = per_step * args.steps / t
@@ -290,6 +289,16 @@ def measure_peaks(torch, lib):
     return out
 
 
+def reduce_max(x: float, dist=None, device=None) -> float:
+    """Max over ranks (timing is the slowest rank's; one process per GPU)."""
+    if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64, device=device or "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 def load_peaks():
     try:
         return json.loads((ROOT / "MEASURED_PEAKS.json").read_text())
@@ -315,7 +324,7 @@ def run_ours(args, W):
     # CPU baseline first (fork-based pool before CUDA is initialised).
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        ips, sample, cores, _ = cpu_measure(cfg, W, args.cpu_seconds)
+        ips, sample, cores, _ = cpu_measure(cfg, W)
         cpu = {"value": ips, "unit": "images/s", "cores": cores, "kind": "port", "sample": sample}
 
     import torch
@@ -401,12 +410,7 @@ def run_ours(args, W):
         torch.cuda.synchronize()
         sustain.append(a0.elapsed_time(a1) * 1e-3)
     clocks = sampler.stop()
-    if dist:
-        t = torch.tensor([elapsed], device="cuda", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed_max = float(t.item())
-    else:
-        elapsed_max = elapsed
+    elapsed_max = reduce_max(elapsed, dist, "cuda")
     value = world * B * K / elapsed_max
 
     # e2e through the public API with host buffers
@@ -445,10 +449,7 @@ def run_ours(args, W):
         q1.record()
         torch.cuda.synchronize()
         et = q0.elapsed_time(q1) * 1e-3
-        if dist:
-            t = torch.tensor([et], device="cuda", dtype=torch.float64)
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            et = float(t.item())
+        et = reduce_max(et, dist, "cuda")
         e2e = {"value": world * B * E / et, "unit": "images/s", "h2d_bytes_per_step": B * 8 + (B * 20 if cfg == "c3"
                                                                                            else 0),
                "d2h_bytes_per_step": B * H * Wd * 3 * 4, "steps": E,

@@ -123,6 +123,12 @@ RINR_API int64_t rinr_last_error_record(void);
  * read_raw(k) for every k.  On success *count = number of records. */
 RINR_API int rinr_archive_validate(const void* bytes, size_t len, int64_t* count);
 
+/* Host-only: global indices of the records rinr_store_create(..., shard_rank,
+ * shard_world, ...) keeps (k % shard_world == shard_rank), after the same full
+ * validation.  Writes up to `cap` indices; *count = shard size. */
+RINR_API int rinr_archive_shard(const void* bytes, size_t len, uint32_t shard_rank, uint32_t shard_world,
+                                int64_t* global_index, int64_t cap, int64_t* count);
+
 /* Parse + validate an archive image held in host memory and upload the
  * records whose index k satisfies k % shard_world == shard_rank to `device`
  * HBM.  Replaces rinr.read(source) (archive.py:395-400) + the materialise step

@@ -20,7 +20,7 @@ AUG_NONE, AUG_OFFSET, AUG_CROP = 0, 1, 2
 FLAG_OVERLAP_PROLOGUE = 1
 
 EXPORTS = (
-    "rinr_abi_version", "rinr_last_error", "rinr_last_error_record", "rinr_archive_validate",
+    "rinr_abi_version", "rinr_last_error", "rinr_last_error_record", "rinr_archive_validate", "rinr_archive_shard",
     "rinr_store_create", "rinr_store_destroy", "rinr_store_info", "rinr_store_record_meta",
     "rinr_dequantize", "rinr_decode",
 )
@@ -61,6 +61,7 @@ def lib() -> C.CDLL:
     L.rinr_last_error.restype = C.c_char_p
     L.rinr_last_error_record.restype = i64
     L.rinr_archive_validate.argtypes = [vp, C.c_size_t, C.POINTER(i64)]
+    L.rinr_archive_shard.argtypes = [vp, C.c_size_t, C.c_uint32, C.c_uint32, vp, i64, C.POINTER(i64)]
     L.rinr_store_create.argtypes = [vp, C.c_size_t, C.c_int, C.c_uint32, C.c_uint32, C.POINTER(vp)]
     L.rinr_store_destroy.argtypes = [vp]
     L.rinr_store_info.argtypes = [vp, C.POINTER(StoreInfo)]
@@ -91,6 +92,19 @@ def archive_validate(data: bytes) -> int:
     arr = host_view(data)
     check(lib().rinr_archive_validate(arr.ctypes.data if arr.size else None, arr.size, C.byref(n)))
     return n.value
+
+
+def archive_shard(data, rank: int, world: int):
+    """Global indices of the records a Store(rank, world) keeps (host-only)."""
+    import numpy as np  # noqa: PLC0415
+    arr = host_view(data)
+    cnt = C.c_int64(0)
+    ptr = arr.ctypes.data if arr.size else None
+    check(lib().rinr_archive_shard(ptr, arr.size, rank, world, None, 0, C.byref(cnt)))
+    out = np.zeros(cnt.value, np.int64)
+    check(lib().rinr_archive_shard(ptr, arr.size, rank, world, out.ctypes.data if out.size else None, out.size,
+                                   C.byref(cnt)))
+    return out
 
 
 def host_view(data):

@@ -269,6 +269,27 @@ int rinr_archive_validate(const void* bytes, size_t len, int64_t* count) {
   return RINR_OK;
 }
 
+int rinr_archive_shard(const void* bytes, size_t len, uint32_t shard_rank, uint32_t shard_world,
+                       int64_t* global_index, int64_t cap, int64_t* count) {
+  clear_error();
+  if (!bytes && len) return set_error(RINR_ERR_INVALID_INPUT, "null archive buffer");
+  if (shard_world < 1 || shard_rank >= shard_world)
+    return set_error(RINR_ERR_INVALID_INPUT, "shard_rank must be in [0, shard_world)");
+  try {
+    ParsedArchive pa;
+    parse_archive(static_cast<const uint8_t*>(bytes), len, shard_rank, shard_world, pa, true);
+    if (count) *count = int64_t(pa.global.size());
+    for (int64_t i = 0; i < int64_t(pa.global.size()) && i < cap && global_index; ++i) global_index[i] = pa.global[i];
+  } catch (const ParseError& e) {
+    int64_t rec = -1;
+    if (e.msg.rfind("record ", 0) == 0) rec = std::atoll(e.msg.c_str() + 7);
+    return set_error(e.code, e.msg, rec);
+  } catch (const std::bad_alloc&) {
+    return set_error(RINR_ERR_OOM, "host allocation failed while parsing");
+  }
+  return RINR_OK;
+}
+
 int rinr_store_create(const void* bytes, size_t len, int device, uint32_t shard_rank, uint32_t shard_world,
                       rinr_store** out) {
   clear_error();
