@@ -310,7 +310,7 @@ int launch_mma_t(const StoreView& sv, const int64_t* ids, int64_t n, const Decod
   // the [2,15,15,3] net against (8,4) (8,2) (16,1) (24,1) (32,1); the wide
   // nets need 8 x 1 to fit their register footprint.
   if constexpr (HID <= 16) return launch_mode<HID, NL, X3, ACC, 16, 2>(sv, ids, n, a, aug, out, status, st, omega, flags);
-  else return launch_mode<HID, NL, X3, ACC, 8, 1>(sv, ids, n, a, aug, out, status, st, omega, flags);
+  else return launch_mode<HID, NL, X3, ACC, 16, 1>(sv, ids, n, a, aug, out, status, st, omega, flags);
 }
 
 template <int HID, int NL>

@@ -46,8 +46,12 @@ struct ImgRegs {
   using C = MmaCfg<HID, NL>;
   static constexpr int K1 = C::NH == 1 ? C::KT : 1;
   static constexpr int N1 = C::NH == 1 ? C::NT : 1;
-  float4 w0[C::KT][4];
-  uint4 bo[C::KT];
+  // Narrow nets keep the layer-0 and output operands in registers; wide nets
+  // (KT > 1) read them from shared memory per group to free ~60 registers.
+  static constexpr bool REG_IO = C::KT == 1;
+  static constexpr int KR = REG_IO ? C::KT : 1;
+  float4 w0[KR][4];
+  uint4 bo[KR];
   float bias_o0, bias_o1;
   uint4 bh1[K1][N1];  // hidden layer 1 fragments (only when it is the only hidden layer)
   float2 bb1[N1];
@@ -67,13 +71,15 @@ struct ImgRegs {
 
   __device__ __forceinline__ void load(const NetView<HID, NL>& net, int lane) {
     const int tq = lane & 3;
+    if constexpr (REG_IO) {
 #pragma unroll
-    for (int t = 0; t < C::KT; ++t)
+      for (int t = 0; t < C::KT; ++t)
 #pragma unroll
-      for (int q = 0; q < 4; ++q)
-        w0[t][q] = reinterpret_cast<const float4*>(net.l0)[16 * t + 2 * tq + (q & 1) + 8 * (q >> 1)];
+        for (int q = 0; q < 4; ++q)
+          w0[t][q] = reinterpret_cast<const float4*>(net.l0)[16 * t + 2 * tq + (q & 1) + 8 * (q >> 1)];
 #pragma unroll
-    for (int t = 0; t < C::KT; ++t) bo[t] = reinterpret_cast<const uint4*>(net.fragO)[t * 32 + lane];
+      for (int t = 0; t < C::KT; ++t) bo[t] = reinterpret_cast<const uint4*>(net.fragO)[t * 32 + lane];
+    }
     bias_o0 = net.biasO[2 * tq];
     bias_o1 = net.biasO[2 * tq + 1];
     if constexpr (C::NH == 1) {
@@ -178,7 +184,9 @@ __device__ __forceinline__ void decode_group(const NetView<HID, NL>& net, const 
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         const bool pad = 16 * t + 8 * (q >> 1) >= HID;  // whole slot is padding (compile time)
-        const float4 w = R.w0[t][q];
+        float4 w;
+        if constexpr (ImgRegs<HID, NL>::REG_IO) w = R.w0[t][q];
+        else w = reinterpret_cast<const float4*>(net.l0)[16 * t + 2 * tq + (q & 1) + 8 * (q >> 1)];
 #pragma unroll
         for (int h = 0; h < 2; ++h) s[h][q] = pad ? 0.0f : sine<ACCURATE>(fmaf(w.y, yr[h], fmaf(w.x, xr[h], w.z)));
       }
@@ -256,9 +264,12 @@ __device__ __forceinline__ void decode_group(const NetView<HID, NL>& net, const 
     float o[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
     for (int t = 0; t < C::KT; ++t) {
-      mma16816(o, ah[bk][t], R.bo[t].x, R.bo[t].y);
-      mma16816(o, ah[bk][t], R.bo[t].z, R.bo[t].w);
-      if constexpr (X3) mma16816(o, al[bk][t], R.bo[t].x, R.bo[t].y);
+      uint4 bo;
+      if constexpr (ImgRegs<HID, NL>::REG_IO) bo = R.bo[t];
+      else bo = reinterpret_cast<const uint4*>(net.fragO)[t * 32 + lane];
+      mma16816(o, ah[bk][t], bo.x, bo.y);
+      mma16816(o, ah[bk][t], bo.z, bo.w);
+      if constexpr (X3) mma16816(o, al[bk][t], bo.x, bo.y);
     }
     // o[0]=(px g, ch 2tq) o[1]=(g, 2tq+1) o[2]=(g+8, 2tq) o[3]=(g+8, 2tq+1)
 #pragma unroll
