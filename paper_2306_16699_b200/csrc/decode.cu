@@ -27,6 +27,7 @@
 
 #include "device_common.cuh"
 #include "persist.cuh"
+#include "tc_decode.cuh"
 
 namespace rinr {
 
@@ -303,14 +304,82 @@ int launch_mode(const StoreView& sv, const int64_t* ids, int64_t n, const Decode
 #undef RINR_LAUNCH
 }
 
+template <int HID, int NL, bool X3, int T, bool INTB>
+int launch_tc_t(const StoreView& sv, const int64_t* ids, int64_t n, const DecodeArgs& a, const float* aug, void* out,
+                int32_t* status, cudaStream_t st, float omega, int flags) {
+  using C = TcCfg<HID, NL, INTB>;
+  constexpr int KW = (HID * HID + 31) / 32 + 1;
+  TcLayout lay{};
+  lay.net_bytes = (C::NET_BYTES + 127) & ~127;
+  lay.tab_floats = ((a.out_w + 3) & ~3) + ((a.out_h + 3) & ~3);
+  lay.rec_bytes = (sv.max_slot_bytes + 16 + 15) & ~15;
+  lay.pfx_words = (NL * 2 * KW + 3) & ~3;
+  lay.tmem_cols = T * C::SLOT_COLS <= 128 ? 128 : (T * C::SLOT_COLS <= 256 ? 256 : 512);
+  static_assert(T * C::SLOT_COLS <= 512, "TMEM holds 512 columns");
+  const bool shared_tab = a.aug == RINR_AUG_NONE;
+  const size_t budget = 227 * 1024;
+  auto need = [&](int maxi, size_t& r0) {
+    r0 = size_t(maxi) * (lay.rec_bytes + size_t(lay.pfx_words) * 4);
+    r0 = (r0 + 1023) & ~size_t(1023);
+    return r0 + size_t(maxi) * lay.net_bytes + size_t(shared_tab ? 1 : maxi) * lay.tab_floats * 4 + T * 8 + 16 +
+           size_t(maxi) * 8 + 64;
+  };
+  const int sms = num_sms();
+  const int64_t tiles = n * ((a.hw + 127) / 128);
+  const int grid = int(tiles < sms ? tiles : sms);
+  const int64_t imgs_per_cta = (n + grid - 1) / grid + 1;
+  int maxi = int(std::min<int64_t>(imgs_per_cta, 8));
+  size_t r0 = 0;
+  while (maxi > 1 && need(maxi, r0) > budget) --maxi;
+  const size_t smem = need(maxi, r0);
+  if (smem > budget) return set_error(RINR_ERR_UNSUPPORTED, "record too large for the tensor-core decode kernel");
+  lay.maxi = maxi;
+  lay.region0 = int(r0);
+  auto kern = decode_tc<HID, NL, X3, T, INTB>;
+  if (!ensure_smem(kern, smem)) return launch_fail("decode_tc smem attribute");
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(4 * T * 32);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  const int overlap = (flags & RINR_FLAG_OVERLAP_PROLOGUE) ? 1 : 0;
+  if (cudaLaunchKernelEx(&cfg, kern, sv, ids, n, a, aug, out, status, omega, lay, overlap) != cudaSuccess)
+    return launch_fail("decode_tc launch");
+  return RINR_OK;
+}
+
+// T = tile slots in flight (4 epilogue warps each); INTB = store-wide
+// "hidden layers are affine8" (no B lo arrays, frees shared memory for slots).
+template <int HID, int NL, bool X3>
+int launch_tc(const StoreView& sv, const int64_t* ids, int64_t n, const DecodeArgs& a, const float* aug, void* out,
+              int32_t* status, cudaStream_t st, float omega, int flags) {
+  if (sv.hidden_int8) return launch_tc_t<HID, NL, X3, 4, true>(sv, ids, n, a, aug, out, status, st, omega, flags);
+  return launch_tc_t<HID, NL, X3, 4, false>(sv, ids, n, a, aug, out, status, st, omega, flags);
+}
+
 template <int HID, int NL, bool X3, bool ACC>
 int launch_mma_t(const StoreView& sv, const int64_t* ids, int64_t n, const DecodeArgs& a, const float* aug, void* out,
                  int32_t* status, cudaStream_t st, float omega, int flags) {
-  // CTA shape = warps x (16-pixel blocks per warp).  16 x 2 measured best for
-  // the [2,15,15,3] net against (8,4) (8,2) (16,1) (24,1) (32,1); the wide
-  // nets need 8 x 1 to fit their register footprint.
-  if constexpr (HID <= 16) return launch_mode<HID, NL, X3, ACC, 16, 2>(sv, ids, n, a, aug, out, status, st, omega, flags);
-  else return launch_mode<HID, NL, X3, ACC, 16, 1>(sv, ids, n, a, aug, out, status, st, omega, flags);
+  if constexpr (HID <= 16) {
+    // CTA shape = warps x (16-pixel blocks per warp): 16 x 2 measured best for
+    // the [2,15,15,3] net against (8,4) (8,2) (16,1) (24,1) (32,1)
+    return launch_mode<HID, NL, X3, ACC, 16, 2>(sv, ids, n, a, aug, out, status, st, omega, flags);
+  } else {
+    if constexpr (!ACC) {
+      // wide nets: tcgen05 + TMEM kernel (RINR_NO_TC=1 selects the mma.sync chain, for A/B comparison)
+      static const bool no_tc = [] {
+        const char* e = std::getenv("RINR_NO_TC");
+        return e && e[0] == '1';
+      }();
+      if (!no_tc) return launch_tc<HID, NL, X3>(sv, ids, n, a, aug, out, status, st, omega, flags);
+    }
+    return launch_mode<HID, NL, X3, ACC, 16, 1>(sv, ids, n, a, aug, out, status, st, omega, flags);
+  }
 }
 
 template <int HID, int NL>

@@ -53,6 +53,7 @@ struct StoreView {
   int32_t max_slot_bytes;   // largest slot (16-B multiple)
   int32_t max_params;
   int32_t max_width;
+  int32_t hidden_int8;      // 1: every hidden layer of every record is affine8 codes
 };
 
 // Slot of record `id`: start and size in bytes.

@@ -80,6 +80,7 @@ static T rd(const uint8_t* p) {
 }
 
 struct ParsedRecord {
+  bool hidden_int8 = true;   // every hidden layer stored as (non-constant) affine8 codes
   size_t body_off = 0;       // offset of the body in the archive image
   uint32_t body_len = 0;     // without CRC
   uint32_t source_h = 0, source_w = 0;
@@ -132,6 +133,7 @@ static void parse_body(const uint8_t* b, size_t len, const std::string& ctx, Par
       throw ParseError{RINR_ERR_INTEGRITY, ctx + ": layer " + std::to_string(l) + " has bad tag/form " +
                                                std::to_string(tag) + "/" + std::to_string(form)};
     bool affine = tag == TAG_A8 || tag == TAG_A16;
+    if (l > 0 && l + 2 < nd && !(tag == TAG_A8 && !cst)) out.hidden_int8 = false;
     if (affine) take(12);
     size_t kept = n;
     if (form != FORM_DENSE) {
@@ -352,6 +354,8 @@ int rinr_store_create(const void* bytes, size_t len, int device, uint32_t shard_
     if (i > 0 && (r.source_h != st->src_h[0] || r.source_w != st->src_w[0])) st->uniform_source = false;
   }
   st->uniform_arch = st->archs.size() <= 1;
+  bool all_int8 = n > 0;
+  for (int64_t i = 0; i < n; ++i) all_int8 = all_int8 && pa.recs[i].hidden_int8;
   const int lstride = lmax + 1;
   const uint32_t hdr = uint32_t((4 * lstride + kRecordAlign - 1) / kRecordAlign * kRecordAlign);
   // Slots: fixed stride when sizes are within 15% of the largest (saves the
@@ -433,6 +437,7 @@ int rinr_store_create(const void* bytes, size_t len, int device, uint32_t shard_
   v.max_slot_bytes = int32_t(max_slot);
   v.max_params = int32_t(st->max_params);
   v.max_width = maxw;
+  v.hidden_int8 = all_int8 ? 1 : 0;
   *out = st.release();
   return RINR_OK;
 }

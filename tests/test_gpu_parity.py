@@ -183,3 +183,29 @@ def test_config3_full_batch_properties(Store):
         std = np.asarray(IMAGENET_STD, np.float32)[:, None, None]
         mse = float(np.mean(((bf[i].float().numpy() - want) * std) ** 2))
         assert 10 * np.log10(1.0 / max(mse, 1e-30)) >= BF16_PSNR_DB
+
+
+@pytest.mark.parametrize("arch_name", ["ARCH_B", "ARCH_C"])
+@pytest.mark.parametrize("quantized", [True, False])
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_wide_nets_all_paths(Store, arch_name, quantized, precision):
+    """Wide uniform nets go to the tcgen05 kernel: the integer-B variant when
+    every hidden layer is affine8, the hi/lo-B variant otherwise."""
+    from paper_2306_16699_b200 import compressor, synth
+    arch = getattr(synth, arch_name)
+    mb = synth.tweak_r1(synth.seeded_batch(arch, range(40, 46), (24, 40)))
+    for b in mb.b:  # non-zero biases exercise the bias path
+        b[:] = np.random.default_rng(3).normal(0, 0.1, b.shape).astype(np.float32)
+    mb = compressor.prune_l1_batch(mb, 0.2)
+    if quantized:
+        mb = compressor.quantize_batch(mb, "affine8")
+    data = synth.archive_bytes(mb)
+    models = O.read_models(data)
+    with Store(data) as st:
+        got = st.decode(torch.arange(6), 24, 40, layout="nhwc", precision=precision).cpu().numpy()
+    want = np.stack(O.decode_batch(models, 24, 40))
+    if precision == "fp32":
+        assert float(np.abs(got - want).max()) <= FP32_TOL
+    else:
+        for i in range(6):
+            assert O.psnr(got[i], want[i]) >= BF16_PSNR_DB
