@@ -53,7 +53,7 @@ def parse_args(argv=None):
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", choices=["c1", "c2", "c3"], default="c2")
+    ap.add_argument("--config", choices=["c1", "c2", "c3", "c4", "c5"], default="c2")
     ap.add_argument("--precision", choices=["fp32", "bf16", "exact"], default=None)
     ap.add_argument("--store-records", type=int, default=None)
     ap.add_argument("--no-e2e", action="store_true")
@@ -64,6 +64,12 @@ def parse_args(argv=None):
 
 
 def workload(cfg: str):
+    if cfg in ("c4", "c5"):
+        return dict(batch=64, h=224, w=224, arch=[2] + [40] * 9 + [3], records=4096, desc=(
+            f"{cfg}: ResNet-18 training step (SGD lr 1e-2, wd 5e-4, bf16 autocast, channels_last; PAPER.md:446) "
+            "fed by on-the-fly decode of 64 affine8+25%-pruned [2,40x9,3] records per GPU at 224x224 with "
+            "random-resized-crop+flip+ImageNet normalise (bf16 NCHW)" +
+            (", DDP over NCCL, store sharded by record" if cfg == "c5" else "")))
     if cfg == "c1":
         return dict(batch=256, h=32, w=32, arch=[2, 15, 15, 3], records=262144, desc=(
             "c1: fp32 dense [2,15,15,3] random-init (R1) records, batch 256, 32x32, fp32 NCHW out"))
@@ -502,9 +508,119 @@ def run_ours(args, W):
     return 0
 
 
+def run_train(args, W):
+    """C4 / C5: end-to-end ResNet-18 training fed by the fused decode."""
+    import torch
+    import torchvision
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2306_16699_b200 import Store
+    from paper_2306_16699_b200.store import IMAGENET_MEAN, IMAGENET_STD, resized_crop_params
+
+    R = args.store_records or W["records"]
+    t0 = time.perf_counter()
+    # every rank holds its own shard: records k with k % world == rank of a world*R store
+    st = Store(store_bytes("c3", R, seed=1000 * rank), device=f"cuda:{local}")
+    build_s = time.perf_counter() - t0
+    B, H, Wd = W["batch"], W["h"], W["w"]
+    K, Wu = args.steps, args.warmup
+    precision = args.precision or "bf16"
+    params = st.decode_params(H, Wd, dtype=torch.bfloat16, precision=precision, aug_mode="crop",
+                              mean=IMAGENET_MEAN, std=IMAGENET_STD)
+    model = torchvision.models.resnet18(num_classes=100).cuda().to(memory_format=torch.channels_last)
+    if dist:
+        model = torch.nn.parallel.DistributedDataParallel(model, device_ids=[local])
+    opt = torch.optim.SGD(model.parameters(), lr=1e-2, momentum=0.9, weight_decay=5e-4)
+    lossf = torch.nn.CrossEntropyLoss()
+    gen = torch.Generator(device="cuda").manual_seed(rank)
+    ids = torch.randint(0, len(st), (Wu + K, B), device="cuda", generator=gen)
+    labels = torch.randint(0, 100, (Wu + K, B), device="cuda", generator=gen)
+    aug = torch.stack([resized_crop_params(B, generator=torch.Generator().manual_seed(1000 * rank + s))
+                       for s in range(Wu + K)]).cuda()
+    xbuf = torch.empty((B, 3, H, Wd), dtype=torch.bfloat16, device="cuda").to(memory_format=torch.contiguous_format)
+
+    def train_step(x, y):
+        with torch.autocast("cuda", dtype=torch.bfloat16):
+            loss = lossf(model(x.contiguous(memory_format=torch.channels_last)), y)
+        opt.zero_grad(set_to_none=True)
+        loss.backward()
+        opt.step()
+        return loss
+
+    def step(k, decode=True):
+        if decode:
+            st.decode(ids[k], out=xbuf, aug=aug[k], params=params, check=False)
+        return train_step(xbuf, labels[k])
+
+    def timed(n0, n, decode=True):
+        if dist:
+            dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for k in range(n0, n0 + n):
+            loss = step(k, decode)
+        e1.record()
+        torch.cuda.synchronize()
+        return reduce_max(e0.elapsed_time(e1) * 1e-3, dist, "cuda"), float(loss.item())
+
+    for k in range(Wu):
+        step(k)
+    torch.cuda.synchronize()
+    sampler = ClockSampler(local)
+    sampler.start()
+    elapsed, loss = timed(Wu, K)
+    clocks = sampler.stop()
+    value = world * B * K / elapsed
+    # decode alone (same launches) and the training step on a static pre-decoded batch
+    torch.cuda.synchronize()
+    d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    d0.record()
+    for k in range(Wu, Wu + K):
+        st.decode(ids[k], out=xbuf, aug=aug[k], params=params, check=False)
+    d1.record()
+    torch.cuda.synchronize()
+    dec_s = d0.elapsed_time(d1) * 1e-3
+    static_s, _ = timed(Wu, K, decode=False)
+    if dist:
+        dist.destroy_process_group()
+    if rank != 0:
+        return 0
+    line = {
+        "metric": "decoded+trained images/sec", "value": value, "unit": "images/s", "n_gpus": world, "steps": K,
+        "warmup": Wu, "ms_per_step": 1e3 * elapsed / K, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
+        "config": {"workload": W["desc"], "batch_per_gpu": B, "store_records_per_gpu": R, "precision": precision,
+                   "parallelism": f"DDP x{world} (NCCL gradient all-reduce), image-sharded store" if world > 1
+                   else "single GPU", "store_build_s": round(build_s, 2)},
+        "decode_ms_per_step": 1e3 * dec_s / K,
+        "decode_share_of_step": dec_s / elapsed,
+        "static_batch_images_per_s": world * B * K / static_s,
+        "final_loss": loss,
+        "gpu_launches": K,
+        "clocks": clocks,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def main(argv=None):
     args = parse_args(argv)
     W = workload(args.config)
+    if args.config in ("c4", "c5"):
+        if args.impl == "reference":
+            rank = int(os.environ.get("RANK", "0"))
+            if rank == 0:
+                print(json.dumps({"impl": "reference", "unavailable": "the reference has no GPU training path "
+                                  "(SPEC.md:8 puts ResNet-18 training out of scope)"}), flush=True)
+            return 0
+        return run_train(args, W)
     if args.impl == "reference":
         return run_reference(args, W)
     return run_ours(args, W)
