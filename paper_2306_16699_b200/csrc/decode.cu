@@ -264,6 +264,7 @@ int launch_persist(const StoreView& sv, const int64_t* ids, int64_t n, const Dec
   if (fixed + per_img > budget) return set_error(RINR_ERR_UNSUPPORTED, "record or output too large for the decode kernel");
   const int sms = num_sms();
   const int64_t groups = n * ((((a.hw + 15) / 16) + NB - 1) / NB);
+  if (groups >= (int64_t(1) << 31)) return set_error(RINR_ERR_INVALID_INPUT, "batch too large for one decode call");
   const int grid = int(groups < sms ? groups : sms);
   const int64_t imgs_per_cta = (n + grid - 1) / grid + 1;
   lay.maxi = int(std::min<int64_t>({int64_t((budget - fixed) / per_img), imgs_per_cta, 64}));
@@ -289,17 +290,22 @@ int launch_persist(const StoreView& sv, const int64_t* ids, int64_t n, const Dec
 template <int HID, int NL, bool X3, bool ACC, int NW, int NB>
 int launch_mode(const StoreView& sv, const int64_t* ids, int64_t n, const DecodeArgs& a, const float* aug, void* out,
                 int32_t* status, cudaStream_t st, float omega, int flags) {
-#define RINR_LAUNCH(AL, ST) \
-  launch_persist<HID, NL, X3, ACC, NW, NB, Mode<AL, ST>>(sv, ids, n, a, aug, out, status, st, omega, flags)
+#define RINR_LAUNCH(AL, ST, IB) \
+  launch_persist<HID, NL, X3, ACC, NW, NB, Mode<AL, ST, IB>>(sv, ids, n, a, aug, out, status, st, omega, flags)
   constexpr int GPX = NB * 16;
   if constexpr (ACC) {
-    return RINR_LAUNCH(false, 0);  // accurate-sine kernels: one generic store path
+    return RINR_LAUNCH(false, 0, false);  // accurate-sine kernels: one generic store path
   } else {
-    if (a.out_w % GPX != 0) return RINR_LAUNCH(false, 0);
-    if (a.layout == RINR_LAYOUT_NCHW && a.dtype == RINR_OUT_F32) return RINR_LAUNCH(true, 1);
-    if (a.layout == RINR_LAYOUT_NCHW && a.dtype == RINR_OUT_BF16) return RINR_LAUNCH(true, 2);
-    if (a.layout == RINR_LAYOUT_NHWC && a.dtype == RINR_OUT_F32) return RINR_LAUNCH(true, 3);
-    return RINR_LAUNCH(true, 0);
+    if (a.out_w % GPX != 0) return RINR_LAUNCH(false, 0, false);
+    if (sv.hidden_int8) {  // store-wide: every hidden layer is affine8 codes
+      if (a.layout == RINR_LAYOUT_NCHW && a.dtype == RINR_OUT_F32) return RINR_LAUNCH(true, 1, true);
+      if (a.layout == RINR_LAYOUT_NCHW && a.dtype == RINR_OUT_BF16) return RINR_LAUNCH(true, 2, true);
+      if (a.layout == RINR_LAYOUT_NHWC && a.dtype == RINR_OUT_F32) return RINR_LAUNCH(true, 3, true);
+    }
+    if (a.layout == RINR_LAYOUT_NCHW && a.dtype == RINR_OUT_F32) return RINR_LAUNCH(true, 1, false);
+    if (a.layout == RINR_LAYOUT_NCHW && a.dtype == RINR_OUT_BF16) return RINR_LAUNCH(true, 2, false);
+    if (a.layout == RINR_LAYOUT_NHWC && a.dtype == RINR_OUT_F32) return RINR_LAUNCH(true, 3, false);
+    return RINR_LAUNCH(true, 0, false);
   }
 #undef RINR_LAUNCH
 }

@@ -102,10 +102,13 @@ struct ImgRegs {
 //             ALIGNED only), 0 any dtype/layout (scalar stores)
 // Each mode is its own kernel instantiation (one large inlined loop per
 // kernel keeps ptxas from spilling).
-template <bool ALIGNED_, int STORE_>
+//   INTB    : every hidden layer of every record in the store is affine8
+//             (integer-code B operand; compile-time, no branch around mma.sync)
+template <bool ALIGNED_, int STORE_, bool INTB_ = false>
 struct Mode {
   static constexpr bool ALIGNED = ALIGNED_;
   static constexpr int STORE = STORE_;
+  static constexpr bool INTB = INTB_;
 };
 
 // Per-lane store addressing, fixed for a launch.
@@ -187,8 +190,15 @@ __device__ __forceinline__ void decode_group(const NetView<HID, NL>& net, const 
         float4 w;
         if constexpr (ImgRegs<HID, NL>::REG_IO) w = R.w0[t][q];
         else w = reinterpret_cast<const float4*>(net.l0)[16 * t + 2 * tq + (q & 1) + 8 * (q >> 1)];
+        if constexpr (ALIGNED) {
+          // the whole group is one image row: omega*(w1*y + b) once per unit
+          const float yb = fmaf(w.y, yr[0], w.z);
 #pragma unroll
-        for (int h = 0; h < 2; ++h) s[h][q] = pad ? 0.0f : sine<ACCURATE>(fmaf(w.y, yr[h], fmaf(w.x, xr[h], w.z)));
+          for (int h = 0; h < 2; ++h) s[h][q] = pad ? 0.0f : sine<ACCURATE>(fmaf(w.x, xr[h], yb));
+        } else {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) s[h][q] = pad ? 0.0f : sine<ACCURATE>(fmaf(w.y, yr[h], fmaf(w.x, xr[h], w.z)));
+        }
       }
       pack_act<X3>(s[0][0], s[0][1], ah[bk][t][0], al[bk][t][0]);
       pack_act<X3>(s[1][0], s[1][1], ah[bk][t][1], al[bk][t][1]);
@@ -200,7 +210,7 @@ __device__ __forceinline__ void decode_group(const NetView<HID, NL>& net, const 
 #pragma unroll 1
   for (int hl = 0; hl < C::NH; ++hl) {
     const uint32_t* fr = net.fragH + hl * C::KT * C::NT * 32 * 4;
-    const bool int_b = C::NH == 1 ? R.int1 : net.modeH[hl] != 0;
+    const bool int_b = M::INTB || (C::NH == 1 ? R.int1 : net.modeH[hl] != 0);
     const float sc = C::NH == 1 ? R.sc1 : net.scaleH[hl];
     float acc[NB][C::NT][4];
 #pragma unroll
@@ -228,8 +238,12 @@ __device__ __forceinline__ void decode_group(const NetView<HID, NL>& net, const 
         }
       }
     };
-    if (int_b) mma_layer(std::false_type{});
-    else mma_layer(std::true_type{});
+    if constexpr (M::INTB) {
+      mma_layer(std::false_type{});
+    } else {
+      if (int_b) mma_layer(std::false_type{});
+      else mma_layer(std::true_type{});
+    }
     float2 bias[C::NT];
 #pragma unroll
     for (int j = 0; j < C::NT; ++j) {
@@ -323,14 +337,17 @@ __device__ __forceinline__ void phase2_loop(const uint32_t* nets, const float* t
   using Net = NetView<HID, NL>;
   constexpr int GPX = NB * 16;
   const StoreLane SL = make_store_lane<NB, M::STORE>(a, lane);
-  int i = (gs + warp) / gpi, within = gs + warp - i * gpi;
+  // each warp takes a contiguous run of groups (few image changes per warp)
+  const int cnt = ge - gs;
+  const int w0g = gs + int((int64_t(cnt) * warp) / NW), w1g = gs + int((int64_t(cnt) * (warp + 1)) / NW);
+  int i = w0g / gpi, within = w0g - i * gpi;
   int cur = -1;
   ImgRegs<HID, NL> R;
   R.set_norm(a, lane);
   Net net(const_cast<uint32_t*>(nets));
   int64_t obase = 0;
 #pragma unroll 1
-  for (int gg = gs + warp; gg < ge; gg += NW) {
+  for (int gg = w0g; gg < w1g; ++gg) {
     if (i != cur) {
       cur = i;
       net = Net(const_cast<uint32_t*>(nets) + i * lay.net_words);
@@ -341,8 +358,10 @@ __device__ __forceinline__ void phase2_loop(const uint32_t* nets, const float* t
     const float* rowy = colx + ((a.out_w + 3) & ~3);
     decode_group<HID, NL, X3, ACCURATE, NB, M>(net, R, colx, rowy, a, out, cimg + i, obase, within * GPX, invW, stage,
                                                SL, lane);
-    within += NW;
-    while (within >= gpi) { within -= gpi; ++i; }
+    if (++within == gpi) {
+      within = 0;
+      ++i;
+    }
   }
 }
 
@@ -375,11 +394,16 @@ __global__ void __launch_bounds__(NW * 32, 1)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nblk = (a.hw + 15) / 16;
   const int gpi = (nblk + NB - 1) / NB;  // groups per image
-  const int64_t total = n * gpi;
-  const int64_t G0 = total * blockIdx.x / gridDim.x, G1 = total * (blockIdx.x + 1) / gridDim.x;
-  if (G0 >= G1) return;
-  const int64_t img0 = G0 / gpi;
-  const int nimg = int((G1 - 1) / gpi - img0 + 1);
+  // CTA group range [G0, G1): 32-bit arithmetic (the launcher guarantees
+  // n * gpi < 2^31; 64-bit divisions here cost ~60 instructions each)
+  const uint32_t total = uint32_t(n) * uint32_t(gpi);
+  const uint32_t qg = total / gridDim.x, rg = total - qg * gridDim.x;
+  const uint32_t G0u = blockIdx.x * qg + min(blockIdx.x, rg);
+  const uint32_t G1u = G0u + qg + (blockIdx.x < rg ? 1u : 0u);
+  const int64_t G0 = G0u, G1 = G1u;
+  if (G0u >= G1u) return;
+  const int64_t img0 = G0u / uint32_t(gpi);
+  const int nimg = int((G1u - 1) / uint32_t(gpi) - uint32_t(img0) + 1);
   float* stage = stagebase + warp * (3 * GPX);
   const float invW = 1.0f / float(a.out_w);
 
