@@ -153,16 +153,13 @@ template <int HID, int NL, bool X3, bool ACCURATE, int NB, class M>
 __device__ __forceinline__ void decode_group(const NetView<HID, NL>& net, const ImgRegs<HID, NL>& R,
                                              const float* colx, const float* rowy, const DecodeArgs& a,
                                              void* __restrict__ out, int64_t img, int64_t obase, int pbase,
-                                             float invW, float* stage, const StoreLane& SL, int lane) {
+                                             int rb, int cb, float* stage, const StoreLane& SL, int lane) {
+  // (rb, cb): row / column of the group's first pixel
   using C = MmaCfg<HID, NL>;
   constexpr int GPX = NB * 16;
   constexpr bool ALIGNED = M::ALIGNED;
   const int g = lane >> 2, tq = lane & 3;
   const int W = a.out_w;
-  int rb = int(float(pbase) * invW);
-  int cb = pbase - rb * W;
-  if (cb >= W) { cb -= W; ++rb; }
-  if (cb < 0) { cb += W; --rb; }
 
   uint32_t ah[NB][C::KT][4], al[NB][C::KT][4];
 #pragma unroll
@@ -341,6 +338,7 @@ __device__ __forceinline__ void phase2_loop(const uint32_t* nets, const float* t
   const int cnt = ge - gs;
   const int w0g = gs + int((int64_t(cnt) * warp) / NW), w1g = gs + int((int64_t(cnt) * (warp + 1)) / NW);
   int i = w0g / gpi, within = w0g - i * gpi;
+  int rb = (within * GPX) / a.out_w, cb = within * GPX - rb * a.out_w;
   int cur = -1;
   ImgRegs<HID, NL> R;
   R.set_norm(a, lane);
@@ -356,10 +354,17 @@ __device__ __forceinline__ void phase2_loop(const uint32_t* nets, const float* t
     }
     const float* colx = shared_tab ? tabs : tabs + i * lay.tab_floats;
     const float* rowy = colx + ((a.out_w + 3) & ~3);
-    decode_group<HID, NL, X3, ACCURATE, NB, M>(net, R, colx, rowy, a, out, cimg + i, obase, within * GPX, invW, stage,
-                                               SL, lane);
+    decode_group<HID, NL, X3, ACCURATE, NB, M>(net, R, colx, rowy, a, out, cimg + i, obase, within * GPX, rb, cb,
+                                               stage, SL, lane);
+    cb += GPX;
+    while (cb >= a.out_w) {
+      cb -= a.out_w;
+      ++rb;
+    }
     if (++within == gpi) {
       within = 0;
+      rb = 0;
+      cb = 0;
       ++i;
     }
   }
@@ -439,75 +444,52 @@ __global__ void __launch_bounds__(NW * 32, 1)
       }
     cp_async_wait_all();
     __syncthreads();
-    // kept-bit prefix tables: one warp per (image, masked layer)
-    for (int q = warp; q < ni * NL; q += NW) {
-      const int i = q / NL, l = q - i * NL;
+    // Dequantise: one warp per (image, layer) task — the layer header is parsed
+    // once, the kept-bit prefix table is built by the same warp, then the
+    // lanes stride over the layer's weights and biases.
+    for (int task = warp; task < ni * NL; task += NW) {
+      const int i = task / NL, l = task - i * NL;
       if (metaid[i] < 0) continue;
       const uint32_t* lo = reinterpret_cast<const uint32_t*>(recs + size_t(i) * lay.rec_bytes);
       const uint8_t* rec = recs + size_t(i) * lay.rec_bytes + sv.hdr_bytes;
       const int fi = l == 0 ? 2 : HID, fo = l == NL - 1 ? 3 : HID;
       const DLayer L = parse_layer(rec, lo[l], lo[l + 1], fi, fo);
+      uint32_t* words = pfx + i * lay.pfx_words + l * 2 * KW;
       if (L.form != FORM_DENSE) {
-        uint32_t* words = pfx + i * lay.pfx_words + l * 2 * KW;
         build_bit_prefix(rec, L, words, words + KW, lane);
+        __syncwarp();
       }
-    }
-    __syncthreads();
-    // dequantise every parameter of every image of the chunk
-    for (int q = tid; q < ni * PALL; q += NT) {
-      const int i = q / PALL;
-      int e = q - i * PALL;
-      if (metaid[i] < 0) continue;
-      int l, o, k;
-      bool is_bias;
-      if (e < P0) {
-        l = 0;
-        is_bias = e >= 2 * HID;
-        o = is_bias ? e - 2 * HID : e / 2;
-        k = is_bias ? 0 : e - 2 * o;
-      } else if (e < P0 + (NL - 2) * PH) {
-        e -= P0;
-        const int h = e / PH;
-        e -= h * PH;
-        l = 1 + h;
-        is_bias = e >= HID * HID;
-        o = is_bias ? e - HID * HID : e / HID;
-        k = is_bias ? 0 : e - HID * o;
-      } else {
-        e -= P0 + (NL - 2) * PH;
-        l = NL - 1;
-        is_bias = e >= 3 * HID;
-        o = is_bias ? e - 3 * HID : e / HID;
-        k = is_bias ? 0 : e - HID * o;
-      }
-      const uint32_t* lo = reinterpret_cast<const uint32_t*>(recs + size_t(i) * lay.rec_bytes);
-      const uint8_t* rec = recs + size_t(i) * lay.rec_bytes + sv.hdr_bytes;
-      const int fi = l == 0 ? 2 : HID, fo = l == NL - 1 ? 3 : HID;
-      const DLayer L = parse_layer(rec, lo[l], lo[l + 1], fi, fo);
-      const uint32_t* words = pfx + i * lay.pfx_words + l * 2 * KW;
       const bool hidden = l > 0 && l < NL - 1;
       const bool int_b = hidden && L.tag == TAG_A8 && !L.cst;
       Net net(nets + i * lay.net_words);
-      if (is_bias) {
-        const float bb = dq_bias(rec, L, o);
-        if (l == 0) net.l0[o * 4 + 2] = __fmul_rn(omega, bb);
-        else if (hidden) net.biasH[(l - 1) * C::NT * 8 + o] = __fmul_rn(omega, bb);
-        else net.biasO[o] = bb;
-        if (hidden && o == 0) {
+      if (l == 0) {
+        for (int j = lane; j < L.n; j += 32)
+          net.l0[(j >> 1) * 4 + (j & 1)] = __fmul_rn(omega, dq_weight(rec, L, words, words + KW, j));
+        for (int o = lane; o < fo; o += 32) net.l0[o * 4 + 2] = __fmul_rn(omega, dq_bias(rec, L, o));
+      } else if (hidden) {
+        uint32_t* fr = net.fragH + (l - 1) * C::KT * C::NT * 32 * 4;
+        if (int_b) {
+          for (int j = lane; j < L.n; j += 32) {
+            const int o = j / HID, k = j - o * HID;
+            Net::put_b(fr, C::NT, k, o, dq_int(rec, L, words, words + KW, j), 0.0f);
+          }
+        } else {
+          for (int j = lane; j < L.n; j += 32) {
+            const int o = j / HID, k = j - o * HID;
+            Net::put_b_split(fr, C::NT, k, o, __fmul_rn(omega, dq_weight(rec, L, words, words + KW, j)));
+          }
+        }
+        for (int o = lane; o < fo; o += 32) net.biasH[(l - 1) * C::NT * 8 + o] = __fmul_rn(omega, dq_bias(rec, L, o));
+        if (lane == 0) {
           net.modeH[l - 1] = int_b ? 1 : 0;
           net.scaleH[l - 1] = int_b ? __double2float_rn(double(omega) * L.scale) : 1.0f;
         }
       } else {
-        const int j = o * fi + k;
-        if (l == 0) {
-          net.l0[o * 4 + k] = __fmul_rn(omega, dq_weight(rec, L, words, words + KW, j));
-        } else if (hidden) {
-          uint32_t* fr = net.fragH + (l - 1) * C::KT * C::NT * 32 * 4;
-          if (int_b) Net::put_b(fr, C::NT, k, o, dq_int(rec, L, words, words + KW, j), 0.0f);
-          else Net::put_b_split(fr, C::NT, k, o, __fmul_rn(omega, dq_weight(rec, L, words, words + KW, j)));
-        } else {
+        for (int j = lane; j < L.n; j += 32) {
+          const int o = j / HID, k = j - o * HID;
           Net::put_b_split(net.fragO, 1, k, o, dq_weight(rec, L, words, words + KW, j));
         }
+        for (int o = lane; o < fo; o += 32) net.biasO[o] = dq_bias(rec, L, o);
       }
     }
     __syncthreads();
