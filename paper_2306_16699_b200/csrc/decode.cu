@@ -281,7 +281,9 @@ int launch_persist(const StoreView& sv, const int64_t* ids, int64_t n, const Dec
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  const int overlap = (flags & RINR_FLAG_OVERLAP_PROLOGUE) ? 1 : 0;
+  // bits 1-2: development knobs (RINR_DEBUG_SKIP=1 skips phase 2, =2 skips the dequant tasks)
+  static const int dbg = [] { const char* e = getenv("RINR_DEBUG_SKIP"); return e ? atoi(e) & 3 : 0; }();
+  const int overlap = ((flags & RINR_FLAG_OVERLAP_PROLOGUE) ? 1 : 0) | (dbg << 1);
   if (cudaLaunchKernelEx(&cfg, kern, sv, ids, n, a, aug, out, status, omega, lay, overlap) != cudaSuccess)
     return launch_fail("decode_persist launch");
   return RINR_OK;

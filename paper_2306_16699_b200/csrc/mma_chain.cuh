@@ -34,6 +34,25 @@ __device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], 
 
 __device__ __forceinline__ uint32_t bf2_bits(__nv_bfloat162 v) { return *reinterpret_cast<uint32_t*>(&v); }
 
+// Blackwell packed fp32 (FFMA2 / FADD2): two IEEE fp32 ops, each rounded as
+// the scalar op would be, in one issue slot.
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rc, rd;\n\tmov.b64 ra, {%2,%3};\n\tmov.b64 rb, {%4,%5};\n\tmov.b64 rc, {%6,%7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0,%1}, rd;}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+__device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2,%3};\n\tmov.b64 rb, {%4,%5};\n\t"
+      "sub.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0,%1}, rd;}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+
 // (x0, x1) -> packed bf16x2 hi and, for the split, lo = bf16(x - f32(hi)).
 // X3 uses a truncation split: hi = top 16 bits (one byte-permute packs the
 // pair), lo = the exact remainder x - hi rounded to bf16; |x - hi - lo| <= 2^-16 |x|.
@@ -42,8 +61,9 @@ __device__ __forceinline__ void pack_act(float x0, float x1, uint32_t& hi, uint3
   if constexpr (X3) {
     const uint32_t u0 = __float_as_uint(x0), u1 = __float_as_uint(x1);
     hi = __byte_perm(u0, u1, 0x7632);
-    lo = bf2_bits(__floats2bfloat162_rn(x0 - __uint_as_float(u0 & 0xffff0000u),
-                                        x1 - __uint_as_float(u1 & 0xffff0000u)));
+    const float2 r = fsub2(make_float2(x0, x1),
+                           make_float2(__uint_as_float(u0 & 0xffff0000u), __uint_as_float(u1 & 0xffff0000u)));
+    lo = bf2_bits(__floats2bfloat162_rn(r.x, r.y));
   } else {
     hi = bf2_bits(__floats2bfloat162_rn(x0, x1));
   }

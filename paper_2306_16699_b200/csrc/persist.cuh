@@ -190,8 +190,9 @@ __device__ __forceinline__ void decode_group(const NetView<HID, NL>& net, const 
         if constexpr (ALIGNED) {
           // the whole group is one image row: omega*(w1*y + b) once per unit
           const float yb = fmaf(w.y, yr[0], w.z);
-#pragma unroll
-          for (int h = 0; h < 2; ++h) s[h][q] = pad ? 0.0f : sine<ACCURATE>(fmaf(w.x, xr[h], yb));
+          const float2 z = ffma2(make_float2(xr[0], xr[1]), make_float2(w.x, w.x), make_float2(yb, yb));
+          s[0][q] = pad ? 0.0f : sine<ACCURATE>(z.x);
+          s[1][q] = pad ? 0.0f : sine<ACCURATE>(z.y);
         } else {
 #pragma unroll
           for (int h = 0; h < 2; ++h) s[h][q] = pad ? 0.0f : sine<ACCURATE>(fmaf(w.y, yr[h], fmaf(w.x, xr[h], w.z)));
@@ -253,13 +254,15 @@ __device__ __forceinline__ void decode_group(const NetView<HID, NL>& net, const 
       for (int t = 0; t < C::KT; ++t) {
         float s[8];
 #pragma unroll
-        for (int e = 0; e < 8; ++e) {
+        for (int e = 0; e < 8; e += 2) {
           const int j = 2 * t + (e >> 2);
           if (j < C::NT) {
-            const float bias_e = (e & 1) ? bias[j].y : bias[j].x;
-            s[e] = sine<ACCURATE>(fmaf(acc[bk][j][e & 3], sc, bias_e));
+            const float2 z =
+                ffma2(make_float2(acc[bk][j][e & 3], acc[bk][j][(e & 3) + 1]), make_float2(sc, sc), bias[j]);
+            s[e] = sine<ACCURATE>(z.x);
+            s[e + 1] = sine<ACCURATE>(z.y);
           } else {
-            s[e] = 0.0f;
+            s[e] = s[e + 1] = 0.0f;
           }
         }
         pack_act<X3>(s[0], s[1], ah[bk][t][0], al[bk][t][0]);
@@ -270,6 +273,7 @@ __device__ __forceinline__ void decode_group(const NetView<HID, NL>& net, const 
     }
   }
   // ---- output layer + epilogue -------------------------------------------------
+  float ov[NB][4];
 #pragma unroll
   for (int bk = 0; bk < NB; ++bk) {
     float o[4] = {0.f, 0.f, 0.f, 0.f};
@@ -284,14 +288,20 @@ __device__ __forceinline__ void decode_group(const NetView<HID, NL>& net, const 
     }
     // o[0]=(px g, ch 2tq) o[1]=(g, 2tq+1) o[2]=(g+8, 2tq) o[3]=(g+8, 2tq+1)
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int odd = e & 1;
-      const int ch = 2 * tq + odd;
-      float v = __saturatef(o[e] + (odd ? R.bias_o1 : R.bias_o0));
-      if (!R.ident) v = __fdiv_rn(__fsub_rn(v, odd ? R.mean1 : R.mean0), odd ? R.std1 : R.std0);
-      if (ch < 3) stage[ch * GPX + 16 * bk + g + 8 * (e >> 1)] = v;
-    }
+    for (int e = 0; e < 4; ++e) ov[bk][e] = __saturatef(o[e] + ((e & 1) ? R.bias_o1 : R.bias_o0));
   }
+  if (!R.ident) {  // one uniform branch per group
+#pragma unroll
+    for (int bk = 0; bk < NB; ++bk)
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        ov[bk][e] = __fdiv_rn(__fsub_rn(ov[bk][e], (e & 1) ? R.mean1 : R.mean0), (e & 1) ? R.std1 : R.std0);
+  }
+#pragma unroll
+  for (int bk = 0; bk < NB; ++bk)
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      if (2 * tq + (e & 1) < 3) stage[(2 * tq + (e & 1)) * GPX + 16 * bk + g + 8 * (e >> 1)] = ov[bk][e];
   __syncwarp();
   // ---- coalesced stores -------------------------------------------------------------
   if constexpr (M::STORE == 1) {
@@ -380,7 +390,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
   constexpr int NT = NW * 32;
   // Without the overlap promise the inputs may come from the preceding kernel:
   // wait for it before reading anything.
-  if (!overlap) pdl_wait();
+  if (!(overlap & 1)) pdl_wait();
   constexpr int GPX = NB * 16;
   // per-image parameter count in the flattened dequant walk (weights + biases)
   constexpr int P0 = 2 * HID + HID, PH = HID * HID + HID, PO = 3 * HID + 3;
@@ -447,7 +457,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
     // Dequantise: one warp per (image, layer) task — the layer header is parsed
     // once, the kept-bit prefix table is built by the same warp, then the
     // lanes stride over the layer's weights and biases.
-    for (int task = warp; task < ni * NL; task += NW) {
+    for (int task = (overlap & 4) ? ni * NL : warp; task < ni * NL; task += NW) {
       const int i = task / NL, l = task - i * NL;
       if (metaid[i] < 0) continue;
       const uint32_t* lo = reinterpret_cast<const uint32_t*>(recs + size_t(i) * lay.rec_bytes);
@@ -495,14 +505,15 @@ __global__ void __launch_bounds__(NW * 32, 1)
     __syncthreads();
     // -------------------------------- phase 2 --------------------------------
     if (c0 == 0) {
-      if (overlap) pdl_wait();  // outputs may still be read/written by the preceding grid
+      if (overlap & 1) pdl_wait();  // outputs may still be read/written by the preceding grid
       pdl_trigger();            // every CTA is resident: the next launch may start its prologue
     }
     const int64_t cbase = cimg * gpi;
     const int gs = int((G0 > cbase ? G0 : cbase) - cbase);
     const int ge = int((G1 < cbase + int64_t(ni) * gpi ? G1 : cbase + int64_t(ni) * gpi) - cbase);
-    phase2_loop<HID, NL, X3, ACCURATE, NW, NB, M>(nets, tabs, lay, shared_tab, a, out, cimg, gs, ge, gpi, invW, stage,
-                                                  warp, lane);
+    if (!(overlap & 2))
+      phase2_loop<HID, NL, X3, ACCURATE, NW, NB, M>(nets, tabs, lay, shared_tab, a, out, cimg, gs, ge, gpi, invW,
+                                                    stage, warp, lane);
     __syncthreads();
   }
 }
