@@ -260,12 +260,13 @@ int launch_persist(const StoreView& sv, const int64_t* ids, int64_t n, const Dec
   const size_t fixed = size_t(NW) * 3 * NB * 16 * 4 + (shared_tab ? size_t(lay.tab_floats) * 4 : 0) + 64;
   const size_t per_img = size_t(lay.net_words) * 4 + size_t(lay.rec_bytes) + size_t(lay.pfx_words) * 4 + 8 +
                          (shared_tab ? 0 : size_t(lay.tab_floats) * 4);
-  const size_t budget = 227 * 1024;
+  constexpr int CPS = 16 / NW;  // CTAs per SM (8-warp CTAs pair up so launches overlap)
+  const size_t budget = (228 * 1024) / CPS - 1024;
   if (fixed + per_img > budget) return set_error(RINR_ERR_UNSUPPORTED, "record or output too large for the decode kernel");
   const int sms = num_sms();
   const int64_t groups = n * ((((a.hw + 15) / 16) + NB - 1) / NB);
   if (groups >= (int64_t(1) << 31)) return set_error(RINR_ERR_INVALID_INPUT, "batch too large for one decode call");
-  const int grid = int(groups < sms ? groups : sms);
+  const int grid = int(groups < int64_t(CPS) * sms ? groups : int64_t(CPS) * sms);
   const int64_t imgs_per_cta = (n + grid - 1) / grid + 1;
   lay.maxi = int(std::min<int64_t>({int64_t((budget - fixed) / per_img), imgs_per_cta, 64}));
   const size_t smem = fixed + size_t(lay.maxi) * per_img;
@@ -282,10 +283,30 @@ int launch_persist(const StoreView& sv, const int64_t* ids, int64_t n, const Dec
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   // bits 1-2: development knobs (RINR_DEBUG_SKIP=1 skips phase 2, =2 skips the dequant tasks)
-  static const int dbg = [] { const char* e = getenv("RINR_DEBUG_SKIP"); return e ? atoi(e) & 3 : 0; }();
+  // bit 3 (=4): print per-CTA phase stamps after a synchronising launch
+  static const int dbg = [] { const char* e = getenv("RINR_DEBUG_SKIP"); return e ? atoi(e) & 15 : 0; }();
   const int overlap = ((flags & RINR_FLAG_OVERLAP_PROLOGUE) ? 1 : 0) | (dbg << 1);
   if (cudaLaunchKernelEx(&cfg, kern, sv, ids, n, a, aug, out, status, omega, lay, overlap) != cudaSuccess)
     return launch_fail("decode_persist launch");
+  if (dbg & 4) {
+    cudaStreamSynchronize(st);
+    static long long h[1024 * 16];
+    cudaMemcpyFromSymbol(h, g_dbg_stamp, sizeof(h));
+    const int pairs[][2] = {{0, 1}, {1, 2}, {2, 3}, {3, 4}, {5, 6}, {6, 7}, {7, 8}, {9, 10}, {10, 11}, {11, 12}};
+    const char* names[] = {"ids+issue", "wait", "dequant", "phase2", "w0 parse", "w0 bits", "w0 values",
+                           "w1 parse", "w1 bits", "w1 values"};
+    fprintf(stderr, "stamps (avg/max cycles over %d CTAs):", grid);
+    for (int q = 0; q < 10; ++q) {
+      double acc = 0, mx = 0;
+      for (int b = 0; b < grid; ++b) {
+        const double d = double(h[b * 16 + pairs[q][1]] - h[b * 16 + pairs[q][0]]);
+        acc += d;
+        mx = std::max(mx, d);
+      }
+      fprintf(stderr, " %s %.0f/%.0f", names[q], acc / grid, mx);
+    }
+    fprintf(stderr, "\n");
+  }
   return RINR_OK;
 }
 
@@ -376,6 +397,7 @@ int launch_mma_t(const StoreView& sv, const int64_t* ids, int64_t n, const Decod
   if constexpr (HID <= 16) {
     // CTA shape = warps x (16-pixel blocks per warp): 16 x 2 measured best for
     // the [2,15,15,3] net against (8,4) (8,2) (16,1) (24,1) (32,1)
+    // (8 x 2 at two CTAs per SM, so consecutive launches overlap, measured 2% slower)
     return launch_mode<HID, NL, X3, ACC, 16, 2>(sv, ids, n, a, aug, out, status, st, omega, flags);
   } else {
     if constexpr (!ACC) {

@@ -106,15 +106,8 @@ __device__ __forceinline__ void build_bit_prefix(const uint8_t* rec, const DLaye
 // with archive.materialize:
 //   affine, not const : kept ? f32(f64(scale) * (f64(code) - f64(zp))) : +0.0
 //   f32 / f16 / const : sparse ? (kept ? value : +0.0) : stored value
-__device__ __forceinline__ float dq_weight(const uint8_t* rec, const DLayer& L, const uint32_t* words,
-                                           const uint32_t* prefix, int j) {
-  bool kept = true;
-  int vi = j;
-  if (L.form != FORM_DENSE) {
-    uint32_t wd = words[j >> 5];
-    kept = (wd >> (j & 31)) & 1u;
-    if (L.form == FORM_SPARSE) vi = int(prefix[j >> 5] + __popc(wd & ((1u << (j & 31)) - 1u)));
-  }
+// Value of a weight entry whose kept bit / value index are known.
+__device__ __forceinline__ float dq_value(const uint8_t* rec, const DLayer& L, bool kept, int vi) {
   const bool affine = L.tag == TAG_A8 || L.tag == TAG_A16;
   if (affine && !L.cst) {
     if (!kept) return 0.0f;
@@ -125,6 +118,91 @@ __device__ __forceinline__ float dq_weight(const uint8_t* rec, const DLayer& L, 
   if (L.form == FORM_SPARSE && !kept) return 0.0f;
   if (L.tag == TAG_F16) return __half2float(__ushort_as_half((unsigned short)ld_u16u(rec, L.vals_off + 2u * vi)));
   return __uint_as_float(ld_u32u(rec, L.vals_off + 4u * vi));
+}
+
+__device__ __forceinline__ float dq_weight(const uint8_t* rec, const DLayer& L, const uint32_t* words,
+                                           const uint32_t* prefix, int j) {
+  bool kept = true;
+  int vi = j;
+  if (L.form != FORM_DENSE) {
+    uint32_t wd = words[j >> 5];
+    kept = (wd >> (j & 31)) & 1u;
+    if (L.form == FORM_SPARSE) vi = int(prefix[j >> 5] + __popc(wd & ((1u << (j & 31)) - 1u)));
+  }
+  return dq_value(rec, L, kept, vi);
+}
+
+// Register-resident kept-bitset of a layer with at most 1024 entries: lane i
+// holds word i (bits past n cleared) and the popcount of words [0, i), so a
+// lookup is two shuffles instead of a shared-memory table.  A dense layer
+// reads as all-kept with prefix 32 i, so one branch-free lookup serves all
+// three forms.
+struct WarpBits {
+  uint32_t w, p;
+};
+
+__device__ __forceinline__ WarpBits warp_bits(const uint8_t* rec, const DLayer& L, int lane) {
+  if (L.form == FORM_DENSE) return WarpBits{0xffffffffu, 32u * uint32_t(lane)};
+  const int nw = (L.n + 31) / 32;
+  uint32_t v = 0;
+  if (lane < nw) {
+    v = ld_u32u(rec, L.bits_off + 4u * uint32_t(lane));
+    const int rem = L.n - 32 * lane;
+    if (rem < 32) v &= (1u << rem) - 1u;  // bytes past the bitset belong to the values
+  }
+  const uint32_t c = __popc(v);
+  uint32_t incl = c;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += t;
+  }
+  return WarpBits{v, incl - c};
+}
+
+// Warp-uniform decode recipe of one layer's values (dq_value without branches).
+struct ValueRecipe {
+  uint32_t vals_off, emask;
+  int esize, zp;
+  bool sparse, affine, f16, zero_unkept;
+  double scale;
+};
+
+__device__ __forceinline__ ValueRecipe value_recipe(const DLayer& L) {
+  ValueRecipe r;
+  r.vals_off = L.vals_off;
+  r.sparse = L.form == FORM_SPARSE;
+  const bool aff_tag = L.tag == TAG_A8 || L.tag == TAG_A16;
+  r.affine = aff_tag && !L.cst;  // const affine layers store exact f32 values
+  r.f16 = L.tag == TAG_F16;
+  r.esize = r.affine ? (L.tag == TAG_A8 ? 1 : 2) : (r.f16 ? 2 : 4);
+  r.emask = r.esize == 1 ? 0xFFu : (r.esize == 2 ? 0xFFFFu : 0xFFFFFFFFu);
+  r.zero_unkept = r.affine || r.sparse;
+  r.zp = L.zp;
+  r.scale = L.scale;
+  return r;
+}
+
+// Entry j of the layer (every lane of the warp must call: shuffles).  INT:
+// the integer code - zero_point of an affine8 layer (exact in bf16).
+template <bool INT>
+__device__ __forceinline__ float value_at(const uint8_t* rec, const ValueRecipe& R, const WarpBits& B, int j) {
+  const uint32_t wd = __shfl_sync(0xffffffffu, B.w, j >> 5);
+  const uint32_t pre = __shfl_sync(0xffffffffu, B.p, j >> 5);
+  const uint32_t bit = uint32_t(j) & 31u;
+  const bool kept = (wd >> bit) & 1u;
+  const uint32_t vi = R.sparse ? pre + __popc(wd & ((1u << bit) - 1u)) : uint32_t(j);
+  if constexpr (INT) {
+    const int code = int(rec[R.vals_off + vi]);
+    return kept ? float(code - R.zp) : 0.0f;
+  } else {
+    const uint32_t raw = ld_u32u(rec, R.vals_off + vi * uint32_t(R.esize));
+    const uint32_t code = raw & R.emask;
+    float x;
+    if (R.affine) x = __double2float_rn(__dmul_rn(R.scale, double(code) - double(R.zp)));
+    else x = R.f16 ? __half2float(__ushort_as_half((unsigned short)code)) : __uint_as_float(raw);
+    return (R.zero_unkept && !kept) ? 0.0f : x;
+  }
 }
 
 __device__ __forceinline__ float dq_bias(const uint8_t* rec, const DLayer& L, int o) {

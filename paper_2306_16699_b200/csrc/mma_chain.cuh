@@ -44,6 +44,14 @@ __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
       : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
   return d;
 }
+__device__ __forceinline__ float2 fadd2_(float2 a, float2 b) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2,%3};\n\tmov.b64 rb, {%4,%5};\n\t"
+      "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0,%1}, rd;}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
 __device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
   float2 d;
   asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2,%3};\n\tmov.b64 rb, {%4,%5};\n\t"
@@ -162,6 +170,32 @@ __device__ __forceinline__ void build_coord_tables(const DecodeArgs& a, const fl
 }
 
 // Affine (code - zero_point) of entry j, or 0 when pruned.
+// B fragment word set of one lane for k-tile t, n-tile j of a layer (row-major
+// (out, in) weights; B[k][n] = W[n][k]): {b0 hi, b1 hi, b0 lo, b1 lo}, b0 =
+// (k = 16t+2tq, +1), b1 = (k + 8, k + 9), n = 8j + g; entries outside
+// (fo, fi) are zero.  INT: integer codes (exact in bf16, lo = 0); else
+// mul * value split into bf16 hi + lo (= NetView::put_b_split).
+template <bool INT>
+__device__ __forceinline__ uint4 frag_words(const uint8_t* rec, const ValueRecipe& R, const WarpBits& B, int fi,
+                                            int fo, int t, int j, float mul, int lane) {
+  const int g = lane >> 2, tq = lane & 3, n = 8 * j + g;
+  float v[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int k = 16 * t + 2 * tq + (q & 1) + 8 * (q >> 1);
+    const bool valid = k < fi && n < fo;
+    const float x = value_at<INT>(rec, R, B, valid ? n * fi + k : 0);
+    v[q] = valid ? (INT ? x : __fmul_rn(mul, x)) : 0.0f;
+  }
+  uint4 r;
+  const __nv_bfloat162 h01 = __floats2bfloat162_rn(v[0], v[1]), h23 = __floats2bfloat162_rn(v[2], v[3]);
+  r.x = bf2_bits(h01);
+  r.y = bf2_bits(h23);
+  r.z = bf2_bits(__floats2bfloat162_rn(v[0] - __low2float(h01), v[1] - __high2float(h01)));
+  r.w = bf2_bits(__floats2bfloat162_rn(v[2] - __low2float(h23), v[3] - __high2float(h23)));
+  return r;
+}
+
 __device__ __forceinline__ float dq_int(const uint8_t* rec, const DLayer& L, const uint32_t* words,
                                         const uint32_t* prefix, int j) {
   bool kept = true;

@@ -276,15 +276,25 @@ __device__ __forceinline__ void decode_group(const NetView<HID, NL>& net, const 
   float ov[NB][4];
 #pragma unroll
   for (int bk = 0; bk < NB; ++bk) {
-    float o[4] = {0.f, 0.f, 0.f, 0.f};
+    // three independent accumulators (hi*Bhi, hi*Blo, lo*Bhi): no dependent HMMA chain
+    float o[4] = {0.f, 0.f, 0.f, 0.f}, o2[4] = {0.f, 0.f, 0.f, 0.f}, o3[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
     for (int t = 0; t < C::KT; ++t) {
       uint4 bo;
       if constexpr (ImgRegs<HID, NL>::REG_IO) bo = R.bo[t];
       else bo = reinterpret_cast<const uint4*>(net.fragO)[t * 32 + lane];
       mma16816(o, ah[bk][t], bo.x, bo.y);
-      mma16816(o, ah[bk][t], bo.z, bo.w);
-      if constexpr (X3) mma16816(o, al[bk][t], bo.x, bo.y);
+      mma16816(o2, ah[bk][t], bo.z, bo.w);
+      if constexpr (X3) mma16816(o3, al[bk][t], bo.x, bo.y);
+    }
+    {
+      const float2 s01 = fadd2_(make_float2(o2[0], o2[1]), make_float2(o3[0], o3[1]));
+      const float2 s23 = fadd2_(make_float2(o2[2], o2[3]), make_float2(o3[2], o3[3]));
+      const float2 t01 = fadd2_(make_float2(o[0], o[1]), s01), t23 = fadd2_(make_float2(o[2], o[3]), s23);
+      o[0] = t01.x;
+      o[1] = t01.y;
+      o[2] = t23.x;
+      o[3] = t23.y;
     }
     // o[0]=(px g, ch 2tq) o[1]=(g, 2tq+1) o[2]=(g+8, 2tq) o[3]=(g+8, 2tq+1)
 #pragma unroll
@@ -354,6 +364,8 @@ __device__ __forceinline__ void phase2_loop(const uint32_t* nets, const float* t
   R.set_norm(a, lane);
   Net net(const_cast<uint32_t*>(nets));
   int64_t obase = 0;
+  const float* colx = tabs;
+  const float* rowy = tabs;
 #pragma unroll 1
   for (int gg = w0g; gg < w1g; ++gg) {
     if (i != cur) {
@@ -361,9 +373,9 @@ __device__ __forceinline__ void phase2_loop(const uint32_t* nets, const float* t
       net = Net(const_cast<uint32_t*>(nets) + i * lay.net_words);
       R.load(net, lane);
       obase = (cimg + i) * 3 * int64_t(a.hw);
+      colx = shared_tab ? tabs : tabs + i * lay.tab_floats;
+      rowy = colx + ((a.out_w + 3) & ~3);
     }
-    const float* colx = shared_tab ? tabs : tabs + i * lay.tab_floats;
-    const float* rowy = colx + ((a.out_w + 3) & ~3);
     decode_group<HID, NL, X3, ACCURATE, NB, M>(net, R, colx, rowy, a, out, cimg + i, obase, within * GPX, rb, cb,
                                                stage, SL, lane);
     cb += GPX;
@@ -380,8 +392,16 @@ __device__ __forceinline__ void phase2_loop(const uint32_t* nets, const float* t
   }
 }
 
+// Development timing (RINR_DEBUG_SKIP bit 2): per-CTA clock64 stamps.
+__device__ long long g_dbg_stamp[1024 * 16];
+#define RINR_STAMP(k) \
+  if ((overlap & 8) && tid == 0 && blockIdx.x < 1024) g_dbg_stamp[blockIdx.x * 16 + (k)] = clock64();
+#define RINR_WSTAMP(w, k) \
+  if ((overlap & 8) && warp == (w) && lane == 0 && task < NW && blockIdx.x < 1024) \
+    g_dbg_stamp[blockIdx.x * 16 + (k)] = clock64();
+
 template <int HID, int NL, bool X3, bool ACCURATE, int NW, int NB, class M>
-__global__ void __launch_bounds__(NW * 32, 1)
+__global__ void __launch_bounds__(NW * 32, 16 / NW)
     decode_persist(StoreView sv, const int64_t* __restrict__ ids, int64_t n, DecodeArgs a,
                    const float* __restrict__ aug, void* __restrict__ out, int32_t* status, float omega,
                    PersistLayout lay, int overlap) {
@@ -396,6 +416,8 @@ __global__ void __launch_bounds__(NW * 32, 1)
   constexpr int P0 = 2 * HID + HID, PH = HID * HID + HID, PO = 3 * HID + 3;
   constexpr int PALL = P0 + (NL - 2) * PH + PO;
   constexpr int KW = (HID * HID + 31) / 32 + 1;  // words of one layer's bitset/prefix table
+  // fragment-owner dequant tasks need every layer's bitset in one warp's registers
+  constexpr bool FRAG_TASKS = HID <= 32;
 
   extern __shared__ __align__(16) uint8_t smem[];
   const bool shared_tab = a.aug == RINR_AUG_NONE;
@@ -422,6 +444,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
   float* stage = stagebase + warp * (3 * GPX);
   const float invW = 1.0f / float(a.out_w);
 
+  RINR_STAMP(0)
   if (shared_tab) build_coord_tables(a, aug, 0, tabs, tabs + ((a.out_w + 3) & ~3), tid, NT);
 
   for (int c0 = 0; c0 < nimg; c0 += lay.maxi) {
@@ -446,7 +469,9 @@ __global__ void __launch_bounds__(NW * 32, 1)
       for (uint32_t k = lane; k < bytes / 16; k += 32) cp_async16(dst + 16 * k, src + 16 * k);
     }
     cp_async_commit();
-    for (int i = tid; i < ni * lay.net_words / 4; i += NT) reinterpret_cast<uint4*>(nets)[i] = make_uint4(0, 0, 0, 0);
+    RINR_STAMP(1)
+    if constexpr (!FRAG_TASKS)
+      for (int i = tid; i < ni * lay.net_words / 4; i += NT) reinterpret_cast<uint4*>(nets)[i] = make_uint4(0, 0, 0, 0);
     if (!shared_tab)
       for (int i = 0; i < ni; ++i) {
         float* tab = tabs + i * lay.tab_floats;
@@ -454,9 +479,88 @@ __global__ void __launch_bounds__(NW * 32, 1)
       }
     cp_async_wait_all();
     __syncthreads();
+    RINR_STAMP(2)
+    // Dequantise straight into MMA fragments: task (image i, part h) with
+    // h = 0 -> layer 0 + output layer, h = 1..NH -> hidden layer h.  Every
+    // lane writes exactly the fragment words it owns (padding included), so
+    // the network image needs no zero fill.
+    if constexpr (FRAG_TASKS) {
+      constexpr int TPI = 1 + C::NH;
+      for (int task = ((overlap & 4) || ((overlap & 16) && warp >= 2)) ? ni * TPI : warp; task < ni * TPI; task += NW) {
+        const int i = task / TPI, h = task - i * TPI;
+        if (metaid[i] < 0) continue;
+        const uint32_t* lo = reinterpret_cast<const uint32_t*>(recs + size_t(i) * lay.rec_bytes);
+        const uint8_t* rec = recs + size_t(i) * lay.rec_bytes + sv.hdr_bytes;
+        Net net(nets + i * lay.net_words);
+        if (h == 0) {
+          RINR_WSTAMP(0, 5)
+          const DLayer L0 = parse_layer(rec, lo[0], lo[1], 2, HID);
+          const DLayer LO = parse_layer(rec, lo[NL - 1], lo[NL], HID, 3);
+          if (L0.form == 99) RINR_WSTAMP(0, 15)
+          RINR_WSTAMP(0, 6)
+          const WarpBits B0 = warp_bits(rec, L0, lane), BO = warp_bits(rec, LO, lane);
+          if (B0.w == 0x12345 && BO.w == 0x1234) RINR_WSTAMP(0, 15)
+          RINR_WSTAMP(0, 7)
+          const ValueRecipe R0 = value_recipe(L0), RO = value_recipe(LO);
+          // layer 0: lane c -> {omega w[c][0], omega w[c][1], omega b[c], 0}
+          {
+            const int c = lane < C::KP ? lane : 0;
+            const float w0 = value_at<false>(rec, R0, B0, c < HID ? 2 * c : 0);
+            const float w1 = value_at<false>(rec, R0, B0, c < HID ? 2 * c + 1 : 0);
+            if (lane < C::KP) {
+              float4 e = make_float4(0.f, 0.f, 0.f, 0.f);
+              if (c < HID) {
+                e.x = __fmul_rn(omega, w0);
+                e.y = __fmul_rn(omega, w1);
+                e.z = __fmul_rn(omega, dq_bias(rec, L0, c));
+              }
+              reinterpret_cast<float4*>(net.l0)[c] = e;
+            }
+          }
+#pragma unroll
+          for (int t = 0; t < C::KT; ++t)
+            reinterpret_cast<uint4*>(net.fragO)[t * 32 + lane] = frag_words<false>(rec, RO, BO, HID, 3, t, 0, 1.0f, lane);
+          if (lane < 8) net.biasO[lane] = lane < 3 ? dq_bias(rec, LO, lane) : 0.0f;
+          RINR_WSTAMP(0, 8)
+        } else {
+          const int l = h;
+          RINR_WSTAMP(1, 9)
+          const DLayer L = parse_layer(rec, lo[l], lo[l + 1], HID, HID);
+          if (L.form == 99) RINR_WSTAMP(1, 15)
+          RINR_WSTAMP(1, 10)
+          const WarpBits B = warp_bits(rec, L, lane);
+          if (B.w == 0x12345) RINR_WSTAMP(1, 15)
+          RINR_WSTAMP(1, 11)
+          const ValueRecipe R = value_recipe(L);
+          const bool int_b = M::INTB || (L.tag == TAG_A8 && !L.cst);
+          uint4* fr = reinterpret_cast<uint4*>(net.fragH + (l - 1) * C::KT * C::NT * 32 * 4);
+          if (int_b) {
+#pragma unroll
+            for (int t = 0; t < C::KT; ++t)
+#pragma unroll
+              for (int j = 0; j < C::NT; ++j)
+                fr[(t * C::NT + j) * 32 + lane] = frag_words<true>(rec, R, B, HID, HID, t, j, omega, lane);
+          } else {
+#pragma unroll
+            for (int t = 0; t < C::KT; ++t)
+#pragma unroll
+              for (int j = 0; j < C::NT; ++j)
+                fr[(t * C::NT + j) * 32 + lane] = frag_words<false>(rec, R, B, HID, HID, t, j, omega, lane);
+          }
+          for (int o = lane; o < C::NT * 8; o += 32)
+            net.biasH[(l - 1) * C::NT * 8 + o] = o < HID ? __fmul_rn(omega, dq_bias(rec, L, o)) : 0.0f;
+          RINR_WSTAMP(1, 12)
+          if (lane == 0) {
+            net.modeH[l - 1] = int_b ? 1 : 0;
+            net.scaleH[l - 1] = int_b ? __double2float_rn(double(omega) * L.scale) : 1.0f;
+          }
+        }
+      }
+    }
     // Dequantise: one warp per (image, layer) task — the layer header is parsed
     // once, the kept-bit prefix table is built by the same warp, then the
     // lanes stride over the layer's weights and biases.
+    if constexpr (!FRAG_TASKS)
     for (int task = (overlap & 4) ? ni * NL : warp; task < ni * NL; task += NW) {
       const int i = task / NL, l = task - i * NL;
       if (metaid[i] < 0) continue;
@@ -503,6 +607,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
       }
     }
     __syncthreads();
+    RINR_STAMP(3)
     // -------------------------------- phase 2 --------------------------------
     if (c0 == 0) {
       if (overlap & 1) pdl_wait();  // outputs may still be read/written by the preceding grid
@@ -515,6 +620,7 @@ __global__ void __launch_bounds__(NW * 32, 1)
       phase2_loop<HID, NL, X3, ACCURATE, NW, NB, M>(nets, tabs, lay, shared_tab, a, out, cimg, gs, ge, gpi, invW,
                                                     stage, warp, lane);
     __syncthreads();
+    RINR_STAMP(4)
   }
 }
 

@@ -24,10 +24,11 @@ def main():
     ap.add_argument("--launches", type=int, default=20)
     ap.add_argument("--records", type=int, default=65536)
     ap.add_argument("--precision", default=None)
+    ap.add_argument("--batch", type=int, default=None)
     a = ap.parse_args()
     W = bench.workload(a.config)
     st = Store(bench.store_bytes(a.config, a.records, seed=0))
-    B, H, Wd = W["batch"], W["h"], W["w"]
+    B, H, Wd = a.batch or W["batch"], W["h"], W["w"]
     ids = torch.randint(0, len(st), (a.launches, B), device="cuda")
     prec = a.precision or ("bf16" if a.config == "c3" else "fp32")
     if a.config == "c3":
