@@ -282,31 +282,12 @@ int launch_persist(const StoreView& sv, const int64_t* ids, int64_t n, const Dec
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  // bits 1-2: development knobs (RINR_DEBUG_SKIP=1 skips phase 2, =2 skips the dequant tasks)
-  // bit 3 (=4): print per-CTA phase stamps after a synchronising launch
-  static const int dbg = [] { const char* e = getenv("RINR_DEBUG_SKIP"); return e ? atoi(e) & 15 : 0; }();
+  // development knob (timing breakdowns only): RINR_DEBUG_SKIP=1 skips phase 2, =2 the dequant, =3 both
+  static const int dbg = [] { const char* e = getenv("RINR_DEBUG_SKIP"); return e ? atoi(e) & 3 : 0; }();
   const int overlap = ((flags & RINR_FLAG_OVERLAP_PROLOGUE) ? 1 : 0) | (dbg << 1);
   if (cudaLaunchKernelEx(&cfg, kern, sv, ids, n, a, aug, out, status, omega, lay, overlap) != cudaSuccess)
     return launch_fail("decode_persist launch");
-  if (dbg & 4) {
-    cudaStreamSynchronize(st);
-    static long long h[1024 * 16];
-    cudaMemcpyFromSymbol(h, g_dbg_stamp, sizeof(h));
-    const int pairs[][2] = {{0, 1}, {1, 2}, {2, 3}, {3, 4}, {5, 6}, {6, 7}, {7, 8}, {9, 10}, {10, 11}, {11, 12}};
-    const char* names[] = {"ids+issue", "wait", "dequant", "phase2", "w0 parse", "w0 bits", "w0 values",
-                           "w1 parse", "w1 bits", "w1 values"};
-    fprintf(stderr, "stamps (avg/max cycles over %d CTAs):", grid);
-    for (int q = 0; q < 10; ++q) {
-      double acc = 0, mx = 0;
-      for (int b = 0; b < grid; ++b) {
-        const double d = double(h[b * 16 + pairs[q][1]] - h[b * 16 + pairs[q][0]]);
-        acc += d;
-        mx = std::max(mx, d);
-      }
-      fprintf(stderr, " %s %.0f/%.0f", names[q], acc / grid, mx);
-    }
-    fprintf(stderr, "\n");
-  }
+
   return RINR_OK;
 }
 

@@ -183,9 +183,19 @@ __device__ __forceinline__ ValueRecipe value_recipe(const DLayer& L) {
   return r;
 }
 
+// Storage kinds with a dedicated straight-line decode (value_at<..., KIND>).
+enum ValueKind { VK_GEN = 0, VK_A8 = 1, VK_F32 = 2 };
+
+__device__ __forceinline__ int value_kind(const DLayer& L) {
+  const bool aff_tag = L.tag == TAG_A8 || L.tag == TAG_A16;
+  if (L.tag == TAG_A8 && !L.cst) return VK_A8;
+  if (L.tag == TAG_F32 || (aff_tag && L.cst)) return VK_F32;  // const affine layers store exact f32
+  return VK_GEN;
+}
+
 // Entry j of the layer (every lane of the warp must call: shuffles).  INT:
 // the integer code - zero_point of an affine8 layer (exact in bf16).
-template <bool INT>
+template <bool INT, int KIND = VK_GEN>
 __device__ __forceinline__ float value_at(const uint8_t* rec, const ValueRecipe& R, const WarpBits& B, int j) {
   const uint32_t wd = __shfl_sync(0xffffffffu, B.w, j >> 5);
   const uint32_t pre = __shfl_sync(0xffffffffu, B.p, j >> 5);
@@ -195,6 +205,13 @@ __device__ __forceinline__ float value_at(const uint8_t* rec, const ValueRecipe&
   if constexpr (INT) {
     const int code = int(rec[R.vals_off + vi]);
     return kept ? float(code - R.zp) : 0.0f;
+  } else if constexpr (KIND == VK_A8) {
+    const uint32_t code = rec[R.vals_off + vi];
+    const float x = __double2float_rn(__dmul_rn(R.scale, double(code) - double(R.zp)));
+    return kept ? x : 0.0f;
+  } else if constexpr (KIND == VK_F32) {
+    const float x = __uint_as_float(ld_u32u(rec, R.vals_off + 4u * vi));
+    return (R.sparse && !kept) ? 0.0f : x;
   } else {
     const uint32_t raw = ld_u32u(rec, R.vals_off + vi * uint32_t(R.esize));
     const uint32_t code = raw & R.emask;

@@ -175,7 +175,7 @@ __device__ __forceinline__ void build_coord_tables(const DecodeArgs& a, const fl
 // (k = 16t+2tq, +1), b1 = (k + 8, k + 9), n = 8j + g; entries outside
 // (fo, fi) are zero.  INT: integer codes (exact in bf16, lo = 0); else
 // mul * value split into bf16 hi + lo (= NetView::put_b_split).
-template <bool INT>
+template <bool INT, int KIND = VK_GEN>
 __device__ __forceinline__ uint4 frag_words(const uint8_t* rec, const ValueRecipe& R, const WarpBits& B, int fi,
                                             int fo, int t, int j, float mul, int lane) {
   const int g = lane >> 2, tq = lane & 3, n = 8 * j + g;
@@ -184,7 +184,7 @@ __device__ __forceinline__ uint4 frag_words(const uint8_t* rec, const ValueRecip
   for (int q = 0; q < 4; ++q) {
     const int k = 16 * t + 2 * tq + (q & 1) + 8 * (q >> 1);
     const bool valid = k < fi && n < fo;
-    const float x = value_at<INT>(rec, R, B, valid ? n * fi + k : 0);
+    const float x = value_at<INT, KIND>(rec, R, B, valid ? n * fi + k : 0);
     v[q] = valid ? (INT ? x : __fmul_rn(mul, x)) : 0.0f;
   }
   uint4 r;

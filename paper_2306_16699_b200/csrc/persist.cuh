@@ -392,14 +392,6 @@ __device__ __forceinline__ void phase2_loop(const uint32_t* nets, const float* t
   }
 }
 
-// Development timing (RINR_DEBUG_SKIP bit 2): per-CTA clock64 stamps.
-__device__ long long g_dbg_stamp[1024 * 16];
-#define RINR_STAMP(k) \
-  if ((overlap & 8) && tid == 0 && blockIdx.x < 1024) g_dbg_stamp[blockIdx.x * 16 + (k)] = clock64();
-#define RINR_WSTAMP(w, k) \
-  if ((overlap & 8) && warp == (w) && lane == 0 && task < NW && blockIdx.x < 1024) \
-    g_dbg_stamp[blockIdx.x * 16 + (k)] = clock64();
-
 template <int HID, int NL, bool X3, bool ACCURATE, int NW, int NB, class M>
 __global__ void __launch_bounds__(NW * 32, 16 / NW)
     decode_persist(StoreView sv, const int64_t* __restrict__ ids, int64_t n, DecodeArgs a,
@@ -443,8 +435,6 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW)
   const int nimg = int((G1u - 1) / uint32_t(gpi) - uint32_t(img0) + 1);
   float* stage = stagebase + warp * (3 * GPX);
   const float invW = 1.0f / float(a.out_w);
-
-  RINR_STAMP(0)
   if (shared_tab) build_coord_tables(a, aug, 0, tabs, tabs + ((a.out_w + 3) & ~3), tid, NT);
 
   for (int c0 = 0; c0 < nimg; c0 += lay.maxi) {
@@ -469,7 +459,6 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW)
       for (uint32_t k = lane; k < bytes / 16; k += 32) cp_async16(dst + 16 * k, src + 16 * k);
     }
     cp_async_commit();
-    RINR_STAMP(1)
     if constexpr (!FRAG_TASKS)
       for (int i = tid; i < ni * lay.net_words / 4; i += NT) reinterpret_cast<uint4*>(nets)[i] = make_uint4(0, 0, 0, 0);
     if (!shared_tab)
@@ -479,34 +468,29 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW)
       }
     cp_async_wait_all();
     __syncthreads();
-    RINR_STAMP(2)
     // Dequantise straight into MMA fragments: task (image i, part h) with
     // h = 0 -> layer 0 + output layer, h = 1..NH -> hidden layer h.  Every
     // lane writes exactly the fragment words it owns (padding included), so
     // the network image needs no zero fill.
     if constexpr (FRAG_TASKS) {
       constexpr int TPI = 1 + C::NH;
-      for (int task = ((overlap & 4) || ((overlap & 16) && warp >= 2)) ? ni * TPI : warp; task < ni * TPI; task += NW) {
+      for (int task = (overlap & 4) ? ni * TPI : warp; task < ni * TPI; task += NW) {
         const int i = task / TPI, h = task - i * TPI;
         if (metaid[i] < 0) continue;
         const uint32_t* lo = reinterpret_cast<const uint32_t*>(recs + size_t(i) * lay.rec_bytes);
         const uint8_t* rec = recs + size_t(i) * lay.rec_bytes + sv.hdr_bytes;
         Net net(nets + i * lay.net_words);
         if (h == 0) {
-          RINR_WSTAMP(0, 5)
           const DLayer L0 = parse_layer(rec, lo[0], lo[1], 2, HID);
           const DLayer LO = parse_layer(rec, lo[NL - 1], lo[NL], HID, 3);
-          if (L0.form == 99) RINR_WSTAMP(0, 15)
-          RINR_WSTAMP(0, 6)
           const WarpBits B0 = warp_bits(rec, L0, lane), BO = warp_bits(rec, LO, lane);
-          if (B0.w == 0x12345 && BO.w == 0x1234) RINR_WSTAMP(0, 15)
-          RINR_WSTAMP(0, 7)
           const ValueRecipe R0 = value_recipe(L0), RO = value_recipe(LO);
           // layer 0: lane c -> {omega w[c][0], omega w[c][1], omega b[c], 0}
-          {
+          auto layer0 = [&](auto kind) {
+            constexpr int K = decltype(kind)::value;
             const int c = lane < C::KP ? lane : 0;
-            const float w0 = value_at<false>(rec, R0, B0, c < HID ? 2 * c : 0);
-            const float w1 = value_at<false>(rec, R0, B0, c < HID ? 2 * c + 1 : 0);
+            const float w0 = value_at<false, K>(rec, R0, B0, c < HID ? 2 * c : 0);
+            const float w1 = value_at<false, K>(rec, R0, B0, c < HID ? 2 * c + 1 : 0);
             if (lane < C::KP) {
               float4 e = make_float4(0.f, 0.f, 0.f, 0.f);
               if (c < HID) {
@@ -516,21 +500,25 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW)
               }
               reinterpret_cast<float4*>(net.l0)[c] = e;
             }
-          }
+          };
+          const int k0 = value_kind(L0);
+          if (k0 == VK_F32) layer0(std::integral_constant<int, VK_F32>{});
+          else layer0(std::integral_constant<int, VK_GEN>{});
+          auto outl = [&](auto kind) {
+            constexpr int K = decltype(kind)::value;
 #pragma unroll
-          for (int t = 0; t < C::KT; ++t)
-            reinterpret_cast<uint4*>(net.fragO)[t * 32 + lane] = frag_words<false>(rec, RO, BO, HID, 3, t, 0, 1.0f, lane);
+            for (int t = 0; t < C::KT; ++t)
+              reinterpret_cast<uint4*>(net.fragO)[t * 32 + lane] =
+                  frag_words<false, K>(rec, RO, BO, HID, 3, t, 0, 1.0f, lane);
+          };
+          const int ko = value_kind(LO);
+          if (ko == VK_F32) outl(std::integral_constant<int, VK_F32>{});
+          else outl(std::integral_constant<int, VK_GEN>{});
           if (lane < 8) net.biasO[lane] = lane < 3 ? dq_bias(rec, LO, lane) : 0.0f;
-          RINR_WSTAMP(0, 8)
         } else {
           const int l = h;
-          RINR_WSTAMP(1, 9)
           const DLayer L = parse_layer(rec, lo[l], lo[l + 1], HID, HID);
-          if (L.form == 99) RINR_WSTAMP(1, 15)
-          RINR_WSTAMP(1, 10)
           const WarpBits B = warp_bits(rec, L, lane);
-          if (B.w == 0x12345) RINR_WSTAMP(1, 15)
-          RINR_WSTAMP(1, 11)
           const ValueRecipe R = value_recipe(L);
           const bool int_b = M::INTB || (L.tag == TAG_A8 && !L.cst);
           uint4* fr = reinterpret_cast<uint4*>(net.fragH + (l - 1) * C::KT * C::NT * 32 * 4);
@@ -541,15 +529,20 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW)
               for (int j = 0; j < C::NT; ++j)
                 fr[(t * C::NT + j) * 32 + lane] = frag_words<true>(rec, R, B, HID, HID, t, j, omega, lane);
           } else {
+            auto hid = [&](auto kind) {
+              constexpr int K = decltype(kind)::value;
 #pragma unroll
-            for (int t = 0; t < C::KT; ++t)
+              for (int t = 0; t < C::KT; ++t)
 #pragma unroll
-              for (int j = 0; j < C::NT; ++j)
-                fr[(t * C::NT + j) * 32 + lane] = frag_words<false>(rec, R, B, HID, HID, t, j, omega, lane);
+                for (int j = 0; j < C::NT; ++j)
+                  fr[(t * C::NT + j) * 32 + lane] = frag_words<false, K>(rec, R, B, HID, HID, t, j, omega, lane);
+            };
+            if (value_kind(L) == VK_F32) hid(std::integral_constant<int, VK_F32>{});
+            else hid(std::integral_constant<int, VK_GEN>{});
           }
-          for (int o = lane; o < C::NT * 8; o += 32)
-            net.biasH[(l - 1) * C::NT * 8 + o] = o < HID ? __fmul_rn(omega, dq_bias(rec, L, o)) : 0.0f;
-          RINR_WSTAMP(1, 12)
+          static_assert(C::NT * 8 <= 32, "one bias entry per lane");
+          if (lane < C::NT * 8)
+            net.biasH[(l - 1) * C::NT * 8 + lane] = lane < HID ? __fmul_rn(omega, dq_bias(rec, L, lane)) : 0.0f;
           if (lane == 0) {
             net.modeH[l - 1] = int_b ? 1 : 0;
             net.scaleH[l - 1] = int_b ? __double2float_rn(double(omega) * L.scale) : 1.0f;
@@ -607,7 +600,6 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW)
       }
     }
     __syncthreads();
-    RINR_STAMP(3)
     // -------------------------------- phase 2 --------------------------------
     if (c0 == 0) {
       if (overlap & 1) pdl_wait();  // outputs may still be read/written by the preceding grid
@@ -620,7 +612,6 @@ __global__ void __launch_bounds__(NW * 32, 16 / NW)
       phase2_loop<HID, NL, X3, ACCURATE, NW, NB, M>(nets, tabs, lay, shared_tab, a, out, cimg, gs, ge, gpi, invW,
                                                     stage, warp, lane);
     __syncthreads();
-    RINR_STAMP(4)
   }
 }
 
