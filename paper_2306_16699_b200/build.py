@@ -24,7 +24,7 @@ HEADERS = [ROOT / "include" / "rinr_b200.h", ROOT / "include" / "rinr_b200_diag.
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3,-fvisibility=hidden",
-         "--expt-relaxed-constexpr", "-Xptxas", "-v"]
+         "--expt-relaxed-constexpr", "-Xptxas", "-v"] + os.environ.get("RINR_EXTRA_NVCC_FLAGS", "").split()
 
 
 def _stale() -> bool:

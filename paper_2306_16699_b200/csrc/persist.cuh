@@ -393,7 +393,7 @@ __device__ __forceinline__ void phase2_loop(const uint32_t* nets, const float* t
 }
 
 template <int HID, int NL, bool X3, bool ACCURATE, int NW, int NB, class M>
-__global__ void __launch_bounds__(NW * 32, 16 / NW)
+__global__ void __launch_bounds__(NW * 32, (NW < 16 ? 16 / NW : 1))
     decode_persist(StoreView sv, const int64_t* __restrict__ ids, int64_t n, DecodeArgs a,
                    const float* __restrict__ aug, void* __restrict__ out, int32_t* status, float omega,
                    PersistLayout lay, int overlap) {
