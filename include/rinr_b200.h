@@ -41,7 +41,9 @@ enum rinr_status {
   RINR_ERR_INTEGRITY = 3,     /* IntegrityError    (errors.py:36-41)       */
   RINR_ERR_CUDA = 4,          /* CUDA runtime failure                      */
   RINR_ERR_OOM = 5,           /* device or host allocation failed          */
-  RINR_ERR_UNSUPPORTED = 6    /* valid record this build cannot decode     */
+  RINR_ERR_UNSUPPORTED = 6,   /* valid record this build cannot decode     */
+  RINR_ERR_STRUCTURAL = 7,    /* StructuralError   (errors.py:28)          */
+  RINR_ERR_NUMERIC = 8        /* NumericError      (errors.py:16)          */
 };
 
 /* Output element type / layout of rinr_decode. */

@@ -20,7 +20,9 @@ What is restated (reference file:line):
   * record parse ........... archive.py:233-275 (layout doc archive.py:1-30)
   * materialize (dequant) .. archive.py:278-325 (integer dequant archive.py:294-301)
   * CRC + reader ........... archive.py:328-400
-  * PSNR ................... metrics.py:23-41
+  * PSNR ................... metrics.py:23-41 (+ u8 path image.py:49-55)
+  * prune_l1 ............... compressor.py:100-152
+  * quantize / codes ....... compressor.py:160-218
 and one operation the reference does not have (SPEC.md:8 puts augmentation
 out of scope), defined by this repo and pinned here so the GPU epilogue has a
 checker: ``augment_coords`` / ``epilogue`` (crop / flip / normalise).
@@ -132,9 +134,15 @@ def to_u8(pixels: np.ndarray) -> np.ndarray:
     return np.floor(v * np.float32(255.0) + np.float32(0.5)).astype(np.uint8)
 
 
-def psnr(a: np.ndarray, b: np.ndarray) -> float:
-    """PSNR with peak 1.0 over normalised floats (metrics.py:23-41)."""
-    mse = float(np.mean((a.astype(np.float64) - b.astype(np.float64)) ** 2))
+def psnr(a: np.ndarray, b: np.ndarray, quantized: bool = False) -> float:
+    """PSNR with peak 1.0 over normalised floats (metrics.py:23-41); the
+    quantized variant goes through image.as_u8 (image.py:49-55) first."""
+    if quantized:
+        pa = to_u8(a).astype(np.float64) / 255.0
+        pb = to_u8(b).astype(np.float64) / 255.0
+    else:
+        pa, pb = a.astype(np.float64), b.astype(np.float64)
+    mse = float(np.mean((pa - pb) ** 2))
     return math.inf if mse == 0.0 else 10.0 * math.log10(1.0 / mse)
 
 
@@ -366,3 +374,85 @@ def flat_params(model: OModel) -> np.ndarray:
         parts.append(layer.w.astype(np.float32).ravel())
         parts.append(layer.b.astype(np.float32).ravel())
     return np.concatenate(parts)
+
+
+# ----------------------------------------------------------------------------
+# Encoder-side transforms (checker for csrc/transforms.cu).
+# ----------------------------------------------------------------------------
+
+class OracleStructuralError(ValueError):
+    """compressor.py:135-137 / 148-149 StructuralError."""
+
+
+def prune_l1(weights: list, masks: list, total_ratio: float, scope: str = "global"):
+    """compressor.py:108-152 on one model given as per-matrix (out, in) f32
+    weights and bool masks; returns (weights, masks) copies."""
+    if not (0.0 <= total_ratio < 1.0):
+        raise ValueError("total_ratio must be in [0, 1)")
+    w = [x.copy() for x in weights]
+    m = [x.copy() for x in masks]
+    if scope == "global":
+        mags = np.concatenate([np.abs(x.ravel()).astype(np.float64) for x in weights])   # 102-104
+        order = np.argsort(mags, kind="stable")
+        k = int(math.floor(total_ratio * mags.size + 0.5))                               # 124
+        flat = np.concatenate([x.ravel() for x in m]).copy()
+        flat[order[:k]] = False
+        off = 0
+        for i in range(len(w)):
+            sz = m[i].size
+            new = flat[off:off + sz].reshape(m[i].shape) & m[i]
+            off += sz
+            if not new.any():
+                raise OracleStructuralError("ratio would zero an entire layer")
+            m[i] = new
+            w[i] = np.multiply(w[i], new)                                                 # 138
+    else:
+        for i in range(len(w)):                                                           # 140-151
+            mags = np.abs(w[i].ravel()).astype(np.float64)
+            k = int(math.floor(total_ratio * mags.size + 0.5))
+            new = m[i].ravel().copy()
+            new[np.argsort(mags, kind="stable")[:k]] = False
+            new = new.reshape(m[i].shape)
+            if not new.any():
+                raise OracleStructuralError("ratio would zero an entire layer")
+            m[i] = new
+            w[i] = np.multiply(w[i], new)
+    return w, m
+
+
+def quantize(weights: list, masks: list, biases: list, bits: int):
+    """compressor.py:160-202: hidden matrices 1..L-2 snapped to the affine
+    grid; returns (weights, {layer: (scale, zero_point, constant)})."""
+    for x, b in zip(weights, biases):
+        if not (np.isfinite(x).all() and np.isfinite(b).all()):
+            raise ArithmeticError("non-finite weights")                                  # 172-174
+    qmax = (1 << bits) - 1
+    w = [x.copy() for x in weights]
+    info = {}
+    for i in range(1, len(w) - 1):
+        kept = w[i][masks[i]].astype(np.float64)
+        if kept.size == 0:
+            info[i] = (1.0, 0, True)
+            continue
+        mn, mx = float(kept.min()), float(kept.max())
+        if mx == mn:
+            info[i] = (1.0, 0, True)
+            continue
+        scale = (mx - mn) / qmax
+        zp = int(np.round(-mn / scale))
+        if not (-(1 << 31) <= zp < (1 << 31)):
+            info[i] = (1.0, 0, True)
+            continue
+        codes = np.clip(np.round(w[i].astype(np.float64) / scale) + zp, 0, qmax)
+        snapped = (scale * (codes - zp)).astype(w[i].dtype)
+        np.multiply(snapped, masks[i], out=snapped)
+        w[i] = snapped
+        info[i] = (scale, zp, False)
+    return w, info
+
+
+def quantize_codes(w: np.ndarray, scale: float, zp: int, bits: int) -> np.ndarray:
+    """compressor.py:205-218 (codes recomputed from the snapped weights)."""
+    qmax = (1 << bits) - 1
+    codes = np.clip(np.round(w.astype(np.float64) / scale) + zp, 0, qmax)
+    return codes.astype(np.uint8 if bits == 8 else np.uint16)

@@ -22,7 +22,7 @@ FLAG_OVERLAP_PROLOGUE = 1
 EXPORTS = (
     "rinr_abi_version", "rinr_last_error", "rinr_last_error_record", "rinr_archive_validate", "rinr_archive_shard",
     "rinr_store_create", "rinr_store_destroy", "rinr_store_info", "rinr_store_record_meta",
-    "rinr_dequantize", "rinr_decode",
+    "rinr_dequantize", "rinr_decode", "rinr_prune_l1", "rinr_quantize", "rinr_psnr",
 )
 
 
@@ -69,6 +69,9 @@ def lib() -> C.CDLL:
                                          C.POINTER(C.c_size_t), C.POINTER(C.c_uint32), C.POINTER(C.c_uint32)]
     L.rinr_dequantize.argtypes = [vp, vp, i64, vp, i64, vp, vp]
     L.rinr_decode.argtypes = [vp, vp, i64, C.POINTER(DecodeParams), vp, vp, vp, vp]
+    L.rinr_prune_l1.argtypes = [vp, C.c_int, i64, vp, vp, vp, C.c_int, vp, vp]
+    L.rinr_quantize.argtypes = [vp, C.c_int, i64, C.c_int, vp, vp, vp, vp, vp, vp, vp, vp, vp]
+    L.rinr_psnr.argtypes = [vp, vp, i64, i64, C.c_int, vp, vp, vp]
     L.rinr_diag_launch.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, C.POINTER(C.c_double)]
     L.rinr_diag_launch.restype = C.c_int
     for name in EXPORTS:

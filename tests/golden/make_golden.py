@@ -163,10 +163,88 @@ def main():
     print("rinr", rinr.__version__, "numpy", np.__version__)
 
 
+def transforms_case():
+    """prune_l1 / quantize / quantize_codes / psnr pinned by the reference
+    (checker for csrc/transforms.cu)."""
+    from rinr import metrics
+    from rinr.image import ImageBuffer
+    out = {}
+    rng = np.random.default_rng(11)
+    cases = []  # (name, model, ratio, scope)
+    for s in range(12):
+        cases.append((f"a{s}", r1(net.init(ARCH_A, 500 + s)), float(rng.uniform(0.0, 0.6)), "global"))
+    # magnitude ties, signed zeros and exact zeros
+    m = r1(net.init(ARCH_A, 600))
+    for l in m.layers:
+        l.w = (np.round(l.w * 64.0) / 64.0).astype(np.float32)
+        l.w[0, :2] = np.float32(-0.0)
+    cases.append(("ties", m, 0.37, "global"))
+    cases.append(("ties_pl", m, 0.37, "per_layer"))
+    cases.append(("zero_ratio", r1(net.init(ARCH_A, 601)), 0.0, "global"))
+    cases.append(("per_layer", r1(net.init(ARCH_A, 602)), 0.5, "per_layer"))
+    cases.append(("structural", r1(net.init(ARCH_A, 603)), 0.999, "global"))
+    cases.append(("archc", r1(net.init(ARCH_C, 604)), 0.25, "global"))
+    names = []
+    for name, m, ratio, scope in cases:
+        names.append(name)
+        out[f"{name}/dims"] = np.array(m.arch.dims, np.int32)
+        out[f"{name}/ratio"] = np.float64(ratio)
+        out[f"{name}/scope"] = np.array(scope)
+        out[f"{name}/w"] = np.concatenate([l.w.ravel() for l in m.layers]).view(np.uint32)
+        out[f"{name}/b"] = np.concatenate([l.b.ravel() for l in m.layers])
+        out[f"{name}/mask"] = np.concatenate([x.ravel() for x in m.mask]).astype(np.uint8)
+        try:
+            p = compressor.prune_l1(m, ratio, scope=scope)
+        except Exception as e:  # noqa: BLE001
+            out[f"{name}/prune_error"] = np.array(type(e).__name__)
+            continue
+        out[f"{name}/pw"] = np.concatenate([l.w.ravel() for l in p.layers]).view(np.uint32)
+        out[f"{name}/pmask"] = np.concatenate([x.ravel() for x in p.mask]).astype(np.uint8)
+        for mode in ("affine8", "affine16"):
+            q = compressor.quantize(p, mode)
+            out[f"{name}/{mode}/w"] = np.concatenate([l.w.ravel() for l in q.layers]).view(np.uint32)
+            lay = sorted(q.quant.layers)
+            out[f"{name}/{mode}/scale"] = np.array([q.quant.layers[i].scale for i in lay], np.float64)
+            out[f"{name}/{mode}/zp"] = np.array([q.quant.layers[i].zero_point for i in lay], np.int64)
+            out[f"{name}/{mode}/const"] = np.array([q.quant.layers[i].constant for i in lay], bool)
+            for i in lay:
+                if not q.quant.layers[i].constant:
+                    out[f"{name}/{mode}/codes{i}"] = compressor.quantize_codes(q, i).ravel().astype(np.uint16)
+    # quantize edge cases on hand-built masks: an all-masked hidden layer
+    # (kept.size == 0) and a constant kept range
+    m = r1(net.init(ARCH_A, 605))
+    m.mask[1][:] = False
+    m.layers[1].w[:] = 0.0
+    m.mask[1][3, 4] = True
+    m.layers[1].w[3, 4] = np.float32(0.25)
+    names.append("qedge")
+    out["qedge/dims"] = np.array(m.arch.dims, np.int32)
+    out["qedge/w"] = np.concatenate([l.w.ravel() for l in m.layers]).view(np.uint32)
+    out["qedge/b"] = np.concatenate([l.b.ravel() for l in m.layers])
+    out["qedge/mask"] = np.concatenate([x.ravel() for x in m.mask]).astype(np.uint8)
+    q = compressor.quantize(m, "affine8")
+    out["qedge/affine8/w"] = np.concatenate([l.w.ravel() for l in q.layers]).view(np.uint32)
+    out["qedge/affine8/const"] = np.array([q.quant.layers[1].constant], bool)
+    out["names"] = np.array(names)
+    # PSNR: decoded images vs perturbed targets, float and u8 paths
+    ims = decoder.decode_batch([_src(r1(net.init(ARCH_A, 700 + s))) for s in range(4)])
+    a = np.stack([im.pixels for im in ims])
+    b = np.clip(a + rng.normal(0, 0.02, a.shape).astype(np.float32), 0, 1).astype(np.float32)
+    b[3] = a[3]
+    out["psnr/a"], out["psnr/b"] = a, b
+    out["psnr/f"] = np.array([metrics.psnr(ImageBuffer(x), ImageBuffer(y)).psnr_db for x, y in zip(a, b)])
+    out["psnr/q"] = np.array([metrics.psnr(ImageBuffer(x), ImageBuffer(y), quantized=True).psnr_db
+                              for x, y in zip(a, b)])
+    np.savez_compressed(OUT / "transforms.npz", **out)
+
+
 def _src(m, h=32, w=32):
     m.source_h, m.source_w = h, w
     return m
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and sys.argv[1:] == ["transforms"]:
+    transforms_case()
+elif __name__ == "__main__":
     main()
+    transforms_case()

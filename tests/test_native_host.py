@@ -15,8 +15,8 @@ from paper_2306_16699_b200 import _native as N
 from paper_2306_16699_b200 import errors
 
 
-def header_symbols():
-    text = (ROOT / "include" / "rinr_b200.h").read_text()
+def header_symbols(names=("rinr_b200.h", "rinr_b200_transforms.h")):
+    text = "".join((ROOT / "include" / h).read_text() for h in names)
     return sorted(set(re.findall(r"RINR_API\s+[\w\s\*]+?\b(rinr_\w+)\s*\(", text)))
 
 
@@ -27,6 +27,8 @@ def test_library_exports_header_symbols():
     for s in syms:
         assert hasattr(lib, s), s
     assert lib.rinr_abi_version() == 1
+    for s in header_symbols(("rinr_b200_diag.h",)):
+        assert hasattr(lib, s), s
 
 
 @pytest.mark.parametrize("case", STORE_CASES)

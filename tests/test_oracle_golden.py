@@ -87,3 +87,41 @@ def test_integrity_errors(golden):
         O.read_models(b"XXXX" + bytes(data[4:]))
     with pytest.raises(O.OracleIntegrityError, match="truncated"):
         O.read_models(bytes(data[:-10]))
+
+
+# ---- encoder-side transforms (compressor.py:100-218, metrics.py:23-41) ---------
+
+def test_transforms_oracle(golden):
+    from transforms_common import case, cat
+    g = golden("transforms")
+    for name in g["names"]:
+        name = str(name)
+        dims, w, m, b = case(g, name)
+        if f"{name}/ratio" in g:
+            ratio, scope = float(g[f"{name}/ratio"]), str(g[f"{name}/scope"])
+            if f"{name}/prune_error" in g:
+                with pytest.raises(O.OracleStructuralError):
+                    O.prune_l1(w, m, ratio, scope)
+                continue
+            w, m = O.prune_l1(w, m, ratio, scope)
+            np.testing.assert_array_equal(cat(w).view(np.uint32), g[f"{name}/pw"])
+            np.testing.assert_array_equal(cat(m).astype(np.uint8), g[f"{name}/pmask"])
+        for mode, bits in (("affine8", 8), ("affine16", 16)):
+            if f"{name}/{mode}/w" not in g:
+                continue
+            qw, info = O.quantize(w, m, b, bits)
+            np.testing.assert_array_equal(cat(qw).view(np.uint32), g[f"{name}/{mode}/w"])
+            lay = sorted(info)
+            np.testing.assert_array_equal([info[i][2] for i in lay], g[f"{name}/{mode}/const"])
+            if f"{name}/{mode}/scale" in g:
+                np.testing.assert_array_equal(np.array([info[i][0] for i in lay]).view(np.uint64),
+                                              g[f"{name}/{mode}/scale"].view(np.uint64))
+                np.testing.assert_array_equal([info[i][1] for i in lay], g[f"{name}/{mode}/zp"])
+            for i in lay:
+                if not info[i][2]:
+                    np.testing.assert_array_equal(O.quantize_codes(qw[i], info[i][0], info[i][1], bits).ravel(),
+                                                  g[f"{name}/{mode}/codes{i}"])
+    a, b2 = g["psnr/a"], g["psnr/b"]
+    for k in range(a.shape[0]):
+        assert O.psnr(a[k], b2[k]) == g["psnr/f"][k]
+        assert O.psnr(a[k], b2[k], quantized=True) == g["psnr/q"][k]

@@ -1,0 +1,34 @@
+"""Shared helpers for the transform parity tests (golden: tests/golden/transforms.npz)."""
+
+import numpy as np
+
+
+def split(flat, dims, dtype=None):
+    """Flat concatenated matrices -> list of (out, in) arrays."""
+    out, off = [], 0
+    for l in range(len(dims) - 1):
+        sz = int(dims[l] * dims[l + 1])
+        x = flat[off:off + sz].reshape(int(dims[l + 1]), int(dims[l]))
+        out.append(x.astype(dtype) if dtype is not None else x)
+        off += sz
+    return out
+
+
+def split_bias(flat, dims):
+    out, off = [], 0
+    for l in range(len(dims) - 1):
+        out.append(flat[off:off + int(dims[l + 1])])
+        off += int(dims[l + 1])
+    return out
+
+
+def case(g, name):
+    dims = g[f"{name}/dims"]
+    w = split(g[f"{name}/w"].view(np.float32), dims)
+    m = split(g[f"{name}/mask"], dims, bool)
+    b = split_bias(g[f"{name}/b"], dims)
+    return dims, w, m, b
+
+
+def cat(mats):
+    return np.concatenate([x.ravel() for x in mats])
