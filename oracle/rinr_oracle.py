@@ -23,6 +23,8 @@ What is restated (reference file:line):
   * PSNR ................... metrics.py:23-41 (+ u8 path image.py:49-55)
   * prune_l1 ............... compressor.py:100-152
   * quantize / codes ....... compressor.py:160-218
+  * init / loss_and_grad ... net.py:152-171, 217-265
+  * Adam / cosine / _train . net.py:268-300, encoder.py:28-30, 66-85
 and one operation the reference does not have (SPEC.md:8 puts augmentation
 out of scope), defined by this repo and pinned here so the GPU epilogue has a
 checker: ``augment_coords`` / ``epilogue`` (crop / flip / normalise).
@@ -456,3 +458,95 @@ def quantize_codes(w: np.ndarray, scale: float, zp: int, bits: int) -> np.ndarra
     qmax = (1 << bits) - 1
     codes = np.clip(np.round(w.astype(np.float64) / scale) + zp, 0, qmax)
     return codes.astype(np.uint8 if bits == 8 else np.uint16)
+
+
+# ----------------------------------------------------------------------------
+# Training (checker for the GPU encoder, csrc/fit.cu).  Models here are plain
+# lists of per-layer f32 arrays: ws[l] (out, in), bs[l] (out,), ms[l] bool.
+# ----------------------------------------------------------------------------
+
+def init_model(dims, seed: int, omega: float = 30.0):
+    """net.init (net.py:152-171): PCG64; layer 0 U(+-1/in), later
+    U(+-sqrt(6/in)/omega), zero biases, all-ones masks."""
+    rng = np.random.default_rng(seed)
+    ws, bs, ms = [], [], []
+    for li, (fi, fo) in enumerate(zip(dims[:-1], dims[1:])):
+        bound = 1.0 / fi if li == 0 else np.sqrt(6.0 / fi) / omega
+        ws.append(rng.uniform(-bound, bound, size=(fo, fi)).astype(np.float32))
+        bs.append(np.zeros(fo, np.float32))
+        ms.append(np.ones((fo, fi), bool))
+    return ws, bs, ms
+
+
+def loss_and_grad(ws, bs, ms, omega: float, coords, targets):
+    """net.py:217-265 with reduction="mean": MSE over the 3n values and
+    analytic gradients through the sine layers; masked gradient entries are 0."""
+    a = coords
+    zs, acts = [], [a]
+    last = len(ws) - 1
+    for i, (w, b) in enumerate(zip(ws, bs)):                                   # 183-202
+        z = a @ w.T + b
+        zs.append(z)
+        a = z if i == last else np.sin(omega * z)
+        acts.append(a)
+    resid = acts[-1] - targets
+    scale = 1.0 / resid.size
+    loss = float((resid.astype(np.float64) ** 2).sum() * scale)
+    gws, gbs = [None] * len(ws), [None] * len(ws)
+    delta = (2.0 * scale) * resid
+    for i in range(len(ws) - 1, -1, -1):                                       # 256-264
+        gw = delta.T @ acts[i]
+        gb = delta.sum(axis=0)
+        np.multiply(gw, ms[i], out=gw)
+        gws[i], gbs[i] = gw, gb
+        if i > 0:
+            delta = (delta @ ws[i]) * (omega * np.cos(omega * zs[i - 1]))
+    return loss, gws, gbs
+
+
+class Adam:
+    """net.Adam (net.py:268-300): f32 moments, bias corrections from Python
+    floats, mask re-applied after every step."""
+
+    def __init__(self, ws, bs, beta1=0.9, beta2=0.999, eps=1e-8):
+        self.beta1, self.beta2, self.eps, self.t = beta1, beta2, eps, 0
+        self.m = [(np.zeros_like(w), np.zeros_like(b)) for w, b in zip(ws, bs)]
+        self.v = [(np.zeros_like(w), np.zeros_like(b)) for w, b in zip(ws, bs)]
+
+    def step(self, ws, bs, ms, gws, gbs, lr: float):
+        self.t += 1
+        c1 = 1.0 - self.beta1 ** self.t
+        c2 = 1.0 - self.beta2 ** self.t
+        for l in range(len(ws)):
+            for j, (p, g) in enumerate(((ws[l], gws[l]), (bs[l], gbs[l]))):
+                g = g.astype(p.dtype, copy=False)
+                mp, vp = self.m[l][j], self.v[l][j]
+                mp *= self.beta1
+                mp += (1.0 - self.beta1) * g
+                vp *= self.beta2
+                vp += (1.0 - self.beta2) * g * g
+                p -= lr * (mp / c1) / (np.sqrt(vp / c2) + self.eps)
+            np.multiply(ws[l], ms[l], out=ws[l])
+
+
+def cosine_lr(lr0: float, t: int, total: int) -> float:
+    """encoder.py:28-30."""
+    return 0.5 * lr0 * (1.0 + math.cos(math.pi * t / total))
+
+
+def train(ws, bs, ms, omega, coords, targets, lr0: float, steps: int):
+    """encoder._train (encoder.py:66-85): full-batch Adam + cosine decay;
+    returns the sampled loss curve (every max(1, steps // 64) steps + final)."""
+    opt = Adam(ws, bs)
+    stride = max(1, steps // 64)
+    curve = []
+    for t in range(steps):
+        loss, gws, gbs = loss_and_grad(ws, bs, ms, omega, coords, targets)
+        if not math.isfinite(loss):
+            raise ArithmeticError(f"loss became non-finite at step {t}")
+        if t % stride == 0:
+            curve.append(loss)
+        opt.step(ws, bs, ms, gws, gbs, cosine_lr(lr0, t, steps))
+    loss, _, _ = loss_and_grad(ws, bs, ms, omega, coords, targets)
+    curve.append(loss)
+    return curve

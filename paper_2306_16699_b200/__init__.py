@@ -9,7 +9,7 @@ kernel used in a training loop.
 from .archive import ArchiveRecord, DatasetArchive, encode_record, serialize, serialize_batch, write
 from .compressor import LayerQuant, ModelBatch, QuantInfo, dequantize, prune_l1, quantize
 from .errors import (BatchItemError, FormatError, IntegrityError, InvalidInputError, NumericError, RinrError,
-                     StructuralError, UnsupportedError)
+                     StructuralError, TrainingError, UnsupportedError)
 from .image import ImageBuffer
 from .net import Architecture, InrModel, LayerWeights, init, param_count, validate_model, weight_count
 
@@ -23,6 +23,9 @@ def __getattr__(name):
                 "CIFAR_MEAN", "CIFAR_STD"):
         from . import store
         return getattr(store, name)
+    if name in ("encoder", "transforms"):
+        import importlib
+        return importlib.import_module(f".{name}", __name__)
     if name in ("decode", "decode_batch", "install"):
         from . import decoder
         return getattr(decoder, name)

@@ -22,7 +22,7 @@ FLAG_OVERLAP_PROLOGUE = 1
 EXPORTS = (
     "rinr_abi_version", "rinr_last_error", "rinr_last_error_record", "rinr_archive_validate", "rinr_archive_shard",
     "rinr_store_create", "rinr_store_destroy", "rinr_store_info", "rinr_store_record_meta",
-    "rinr_dequantize", "rinr_decode", "rinr_prune_l1", "rinr_quantize", "rinr_psnr",
+    "rinr_dequantize", "rinr_decode", "rinr_prune_l1", "rinr_quantize", "rinr_psnr", "rinr_fit", "rinr_fit_render",
 )
 
 
@@ -35,6 +35,11 @@ class StoreInfo(C.Structure):
         ("max_param_count", C.c_int64), ("max_record_bytes", C.c_int64), ("device_bytes", C.c_int64),
         ("uniform_source", C.c_int32), ("source_h", C.c_uint32), ("source_w", C.c_uint32),
     ]
+
+
+class FitParams(C.Structure):  # rinr_fit_params_t (include/rinr_b200_encoder.h)
+    _fields_ = [("h", C.c_int32), ("w", C.c_int32), ("steps", C.c_int32), ("sin_mode", C.c_int32),
+                ("lr0", C.c_double), ("omega", C.c_double), ("curve_cap", C.c_int32)]
 
 
 class DecodeParams(C.Structure):
@@ -72,6 +77,8 @@ def lib() -> C.CDLL:
     L.rinr_prune_l1.argtypes = [vp, C.c_int, i64, vp, vp, vp, C.c_int, vp, vp]
     L.rinr_quantize.argtypes = [vp, C.c_int, i64, C.c_int, vp, vp, vp, vp, vp, vp, vp, vp, vp]
     L.rinr_psnr.argtypes = [vp, vp, i64, i64, C.c_int, vp, vp, vp]
+    L.rinr_fit.argtypes = [vp, C.c_int, i64, vp, vp, vp, vp, C.POINTER(FitParams), vp, vp, vp, vp, vp, vp]
+    L.rinr_fit_render.argtypes = [vp, C.c_int, i64, vp, vp, C.c_int32, C.c_int32, C.c_double, C.c_int32, vp, vp]
     L.rinr_diag_launch.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, C.POINTER(C.c_double)]
     L.rinr_diag_launch.restype = C.c_int
     for name in EXPORTS:

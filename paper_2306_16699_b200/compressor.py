@@ -214,6 +214,44 @@ def dequantize(model):
     return out
 
 
+@dataclass(frozen=True)
+class PruneSchedule:
+    """Piecewise-linear PSNR -> total prune ratio map with saturation
+    (compressor.py:20-32)."""
+
+    name: str
+    below: float
+    pieces: tuple
+    above: float
+
+
+SCHEDULES = {  # compressor.py:36-40
+    "cifar": PruneSchedule("cifar", below=0.0, pieces=((30.0, 35.0, 0.05, -1.5),), above=0.25),
+    "large": PruneSchedule("large", below=0.2, pieces=((35.0, 40.0, 0.04, -1.2),), above=0.4),
+}
+
+
+def get_schedule(name: str) -> PruneSchedule:
+    try:
+        return SCHEDULES[name]
+    except KeyError:
+        raise InvalidInputError(f"unknown schedule {name!r}; have {sorted(SCHEDULES)}") from None
+
+
+def dynamic_ratio(schedule: PruneSchedule, psnr: float) -> float:
+    """compressor.py:50-65."""
+    if math.isnan(psnr):
+        raise InvalidInputError("psnr is NaN")
+    if psnr == math.inf:
+        return schedule.above
+    for lo, hi, slope, intercept in schedule.pieces:
+        if psnr < lo:
+            break
+        if psnr <= hi:
+            return slope * psnr + intercept
+    return schedule.below if psnr < schedule.pieces[0][0] else schedule.above
+
+
 def dynamic_ratio_cifar(psnr: float) -> float:
     """The reference's 'cifar' PSNR->ratio schedule (compressor.py:37-65),
     used only to draw realistic per-record prune ratios for synthetic stores."""

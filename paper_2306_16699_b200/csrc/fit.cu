@@ -1,0 +1,525 @@
+// Batched SIREN fitting: encoder._train
+// (encoder.py:66-85) = full-batch Adam (net.py:268-300) over
+// net.loss_and_grad (net.py:217-265), one CTA per image, every step of a
+// round inside one launch.
+//
+// Architecture (2, H, H, 3), 8 <= H <= 16, omega from the record.  Per step:
+//   1. thread = pixel: forward (FFMA + sin/cos) and backward (deltas) in
+//      fp32 registers, the loss accumulated in f64 (resid.astype(f64)**2);
+//   2. each warp stages its 32 pixels' (a0, a1, d0, d1, d2, x, y) in shared
+//      memory, then the lanes reduce the outer products over those pixels in
+//      one uniform instruction stream.  Lanes 0..15 own W1[o][0..7] plus
+//      W0[o][:] / b0 / b1; lanes 16..31 own W1[o][8..] plus W2[:][o] (and b2),
+//      with o = lane % 16;
+//   3. cross-warp sums in shared memory, then the Adam update in numpy's f32
+//      operation order, with the mask re-applied.
+// Shared memory holds the weights (compute copy, padded rows), Adam moments,
+// masks, per-warp partial gradients and the staging tiles: about 180 KB, one CTA per SM.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+#include <string>
+
+#include "../../include/rinr_b200_encoder.h"
+#include "device_common.cuh"
+#include "rinr_internal.h"
+
+namespace rinr {
+namespace {
+
+constexpr int kFitWarps = 16;
+constexpr int kFitThreads = kFitWarps * 32;
+constexpr int kStage = 76;  // floats per staged pixel (stride 76: conflict-free STS.128)
+// staged pixel: a0 [0,16) a1 [16,32) d1 [32,48) d0 [48,64) d2 [64,68) (x, y) [68,70)
+constexpr int SA0 = 0, SA1 = 16, SD1 = 32, SD0 = 48, SD2 = 64, SXY = 68;
+
+template <int H>
+struct FitLayout {
+  // canonical parameter order = transform layout: W0 [H][2], W1 [H][H], W2 [3][H] | b0, b1, b2
+  static constexpr int P = 2 * H + H * H + 3 * H;
+  static constexpr int PB = 2 * H + 3;
+  static constexpr int NPAR = P + PB;
+  static constexpr int NPAR_PAD = (NPAR + 3) & ~3;
+  // shared compute copy (padded rows)
+  static constexpr int W0S = 0, W1S = 32, W2S = 32 + 256, B0S = W2S + 64, B1S = B0S + 16, B2S = B1S + 16;
+  static constexpr int WS = B2S + 16;
+  __device__ static int slot(int p) {
+    if (p < 2 * H) return W0S + p;  // row o = p/2 of 2 floats
+    p -= 2 * H;
+    if (p < H * H) return W1S + (p / H) * 16 + p % H;
+    p -= H * H;
+    if (p < 3 * H) return W2S + (p / H) * 16 + p % H;
+    p -= 3 * H;
+    if (p < H) return B0S + p;
+    p -= H;
+    if (p < H) return B1S + p;
+    return B2S + (p - H);
+  }
+  static constexpr size_t smem_bytes() {
+    return sizeof(float) * (size_t(WS) + 2 * NPAR_PAD + ((P + 3) & ~3) + size_t(kFitWarps) * NPAR_PAD +
+                            size_t(kFitWarps) * 32 * kStage) +
+           sizeof(double) * kFitWarps;
+  }
+};
+
+struct FitArgs {
+  int64_t n;
+  float* w;
+  float* b;
+  const uint8_t* mask;
+  const float* images;
+  int h, wd, hw, steps, cap;
+  double inv_wm1, inv_hm1;
+  double lr0, omega;
+  double* curve;
+  int32_t* status;
+  float* grad_w;
+  float* grad_b;
+  double* loss0;
+};
+
+template <bool ACC>
+__device__ __forceinline__ void sincos_(float u, float& s, float& c) {
+  if constexpr (ACC) sincosf(u, &s, &c);
+  else __sincosf(u, &s, &c);
+}
+
+// Weights are read with volatile vector loads: ptxas may neither hoist nor
+// merge them, so the ~300 loop-invariant weights are re-read per pixel (one
+// LDS.128 per 4 weights, broadcast) instead of being pinned in registers
+// across the pixel loop, which would spill.
+__device__ __forceinline__ float4 wld4(const float* p) {
+  float4 v;
+  asm volatile("ld.volatile.shared.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(static_cast<unsigned>(__cvta_generic_to_shared(p))));
+  return v;
+}
+
+template <int H>
+__device__ __forceinline__ void wrow(const float* p, float (&r)[16]) {
+#pragma unroll
+  for (int k = 0; k < 16; k += 4) {
+    if (k < H) {
+      const float4 v = wld4(p + k);
+      r[k] = v.x;
+      r[k + 1] = v.y;
+      r[k + 2] = v.z;
+      r[k + 3] = v.w;
+    }
+  }
+}
+
+// Per-pixel forward (+ backward when BWD): a0/c0/a1/c1 (c = omega cos(omega z));
+// on return of the backward, c1 holds d1 and c0 holds d0.
+template <int H, bool ACC, bool BWD>
+__device__ __forceinline__ void pixel_pass(const float* __restrict__ ws, float x, float y, const float* tg, float om,
+                                           float s2, float (&a0)[16], float (&c0)[16], float (&a1)[16],
+                                           float (&c1)[16], float (&d2)[3], float (&out)[3], double& lp) {
+  using L = FitLayout<H>;
+  float r[16], bb[16];
+  // layer 0: 2 -> H (W0 rows are float2 pairs: 8 rows per 4 loads)
+  wrow<H>(ws + L::B0S, bb);
+#pragma unroll
+  for (int o0 = 0; o0 < H; o0 += 2) {
+    const float4 w = wld4(ws + L::W0S + 2 * o0);  // rows o0, o0+1
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int o = o0 + h;
+      if (o < H) {
+        const float wx = h ? w.z : w.x, wy = h ? w.w : w.y;
+        const float z = __fadd_rn(fmaf(y, wy, __fmul_rn(x, wx)), bb[o]);
+        float s, c;
+        sincos_<ACC>(__fmul_rn(om, z), s, c);
+        a0[o] = s;
+        c0[o] = __fmul_rn(om, c);
+      }
+    }
+  }
+  // layer 1: H -> H
+  wrow<H>(ws + L::B1S, bb);
+#pragma unroll
+  for (int o = 0; o < H; ++o) {
+    wrow<H>(ws + L::W1S + 16 * o, r);
+    float acc = 0.0f;
+#pragma unroll
+    for (int k = 0; k < H; ++k) acc = fmaf(a0[k], r[k], acc);
+    float s, c;
+    sincos_<ACC>(__fmul_rn(om, __fadd_rn(acc, bb[o])), s, c);
+    a1[o] = s;
+    c1[o] = __fmul_rn(om, c);
+  }
+  // layer 2: H -> 3 (affine)
+  const float4 b2 = wld4(ws + L::B2S);
+#pragma unroll
+  for (int j = 0; j < 3; ++j) {
+    wrow<H>(ws + L::W2S + 16 * j, r);
+    float acc = 0.0f;
+#pragma unroll
+    for (int k = 0; k < H; ++k) acc = fmaf(a1[k], r[k], acc);
+    out[j] = __fadd_rn(acc, j == 0 ? b2.x : (j == 1 ? b2.y : b2.z));
+  }
+  if constexpr (BWD) {
+#pragma unroll
+    for (int j = 0; j < 3; ++j) {
+      const float e = __fsub_rn(out[j], tg[j]);
+      lp += double(e) * double(e);
+      d2[j] = __fmul_rn(s2, e);  // (2.0 * scale) * resid
+    }
+    // d1 = (d2 @ W2) * c1
+    float g[16];
+    wrow<H>(ws + L::W2S, r);
+#pragma unroll
+    for (int k = 0; k < H; ++k) g[k] = __fmul_rn(d2[0], r[k]);
+#pragma unroll
+    for (int j = 1; j < 3; ++j) {
+      wrow<H>(ws + L::W2S + 16 * j, r);
+#pragma unroll
+      for (int k = 0; k < H; ++k) g[k] = fmaf(d2[j], r[k], g[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < H; ++k) c1[k] = __fmul_rn(g[k], c1[k]);
+    // d0 = (d1 @ W1) * c0, row-outer so each W1 row is 4 vector loads
+#pragma unroll
+    for (int k = 0; k < H; ++k) g[k] = 0.0f;
+#pragma unroll
+    for (int o = 0; o < H; ++o) {
+      wrow<H>(ws + L::W1S + 16 * o, r);
+#pragma unroll
+      for (int k = 0; k < H; ++k) g[k] = fmaf(c1[o], r[k], g[k]);
+    }
+#pragma unroll
+    for (int k = 0; k < H; ++k) c0[k] = __fmul_rn(g[k], c0[k]);
+  }
+}
+
+template <int H, bool ACC>
+__global__ void __launch_bounds__(kFitThreads, 1) fit_kernel(FitArgs A) {
+  using L = FitLayout<H>;
+  extern __shared__ __align__(16) float sm[];
+  float* ws = sm;
+  float* mo = ws + L::WS;
+  float* ve = mo + L::NPAR_PAD;
+  float* mk = ve + L::NPAR_PAD;
+  float* part = mk + ((L::P + 3) & ~3);
+  float* stage = part + kFitWarps * L::NPAR_PAD;
+  double* lossw = reinterpret_cast<double*>(stage + kFitWarps * 32 * kStage);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int64_t m = blockIdx.x;
+  float* gw = A.w + m * L::P;
+  float* gb = A.b + m * L::PB;
+
+  for (int i = tid; i < L::WS; i += kFitThreads) ws[i] = 0.0f;
+  __syncthreads();
+  for (int p = tid; p < L::NPAR; p += kFitThreads) {
+    ws[L::slot(p)] = p < L::P ? gw[p] : gb[p - L::P];
+    mo[p] = 0.0f;
+    ve[p] = 0.0f;
+    if (p < L::P) mk[p] = A.mask[m * L::P + p] ? 1.0f : 0.0f;
+  }
+  __syncthreads();
+
+  const int HW = A.hw, nchunks = (HW + 31) / 32;
+  const double scale = 1.0 / (3.0 * double(HW));  // 1.0 / resid.size
+  const float s2 = float(2.0 * scale);
+  const float om = float(A.omega);
+  const int stride = A.steps / 64 > 1 ? A.steps / 64 : 1;
+  const float* img = A.images + m * int64_t(HW) * 3;
+  float* st = stage + warp * 32 * kStage;
+  const int o16 = lane & 15;
+  const bool hi_half = lane >= 16;
+  int slot_c = 0;
+  int32_t status = 0;
+
+  for (int t = 0; t <= A.steps; ++t) {
+    // t == steps: the final forward-only loss (encoder.py:84), except for the
+    // loss_and_grad hook (steps == 0 with gradient outputs)
+    const bool last = t == A.steps && !(A.grad_w && A.steps == 0);
+    // this warp's partial gradient row (canonical order), summed over its chunks
+    float* pw = part + warp * L::NPAR_PAD;
+    if (!last)
+      for (int i = lane; i < L::NPAR_PAD; i += 32) pw[i] = 0.0f;
+    __syncwarp();
+    double lp = 0.0;
+    for (int ch = warp; ch < nchunks; ch += kFitWarps) {
+      const int px = ch * 32 + lane;
+      const bool valid = px < HW;
+      const int pr = valid ? px / A.wd : 0, pc = valid ? px - pr * A.wd : 0;
+      const float x = grid_coord(pc, A.wd, A.inv_wm1), y = grid_coord(pr, A.h, A.inv_hm1);
+      float tg[3] = {0.f, 0.f, 0.f};
+      if (valid) {
+        tg[0] = img[3 * px];
+        tg[1] = img[3 * px + 1];
+        tg[2] = img[3 * px + 2];
+      }
+      float a0[16], c0[16], a1[16], c1[16], d2[3], out[3];
+      double lpx = 0.0;
+      pixel_pass<H, ACC, true>(ws, x, y, tg, om, s2, a0, c0, a1, c1, d2, out, lpx);
+      if (valid) lp += lpx;
+      if (last) continue;
+      if (!valid) {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) c0[k] = c1[k] = 0.0f;
+        d2[0] = d2[1] = d2[2] = 0.0f;
+      }
+      float* row = st + lane * kStage;
+#pragma unroll
+      for (int k = 0; k < 16; k += 4) {
+        *reinterpret_cast<float4*>(row + SA0 + k) = make_float4(a0[k], a0[k + 1], a0[k + 2], a0[k + 3]);
+        *reinterpret_cast<float4*>(row + SA1 + k) = make_float4(a1[k], a1[k + 1], a1[k + 2], a1[k + 3]);
+        *reinterpret_cast<float4*>(row + SD1 + k) = make_float4(c1[k], c1[k + 1], c1[k + 2], c1[k + 3]);
+        *reinterpret_cast<float4*>(row + SD0 + k) = make_float4(c0[k], c0[k + 1], c0[k + 2], c0[k + 3]);
+      }
+      *reinterpret_cast<float4*>(row + SD2) = make_float4(d2[0], d2[1], d2[2], 0.0f);
+      *reinterpret_cast<float4*>(row + SXY) = make_float4(x, y, 0.0f, 0.0f);
+      __syncwarp();
+      const int nq = HW - ch * 32 < 32 ? HW - ch * 32 : 32;
+      // per-lane accumulators live only for this chunk (uniform stream, see header)
+      float g8[8], g3[3], gq[3], gp = 0.0f, gu = 0.0f;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) g8[k] = 0.0f;
+#pragma unroll
+      for (int j = 0; j < 3; ++j) g3[j] = gq[j] = 0.0f;
+      // lanes < 16: u = d1[o], vec = a0[0..7], p = d0[o], q = (x, y, 0)
+      // lanes >= 16: u = d1[o], vec = a0[8..15], p = a1[o], q = d2[0..2]
+      const int vo = hi_half ? SA0 + 8 : SA0;
+      const int po = hi_half ? SA1 + o16 : SD0 + o16;
+      const int qo = hi_half ? SD2 : SXY;
+      for (int q = 0; q < nq; ++q) {
+        const float* r = st + q * kStage;
+        const float u = r[SD1 + o16];
+        const float4 v0 = *reinterpret_cast<const float4*>(r + vo);
+        const float4 v1 = *reinterpret_cast<const float4*>(r + vo + 4);
+        const float p = r[po];
+        const float4 qq = *reinterpret_cast<const float4*>(r + qo);
+        g8[0] = fmaf(u, v0.x, g8[0]);
+        g8[1] = fmaf(u, v0.y, g8[1]);
+        g8[2] = fmaf(u, v0.z, g8[2]);
+        g8[3] = fmaf(u, v0.w, g8[3]);
+        g8[4] = fmaf(u, v1.x, g8[4]);
+        g8[5] = fmaf(u, v1.y, g8[5]);
+        g8[6] = fmaf(u, v1.z, g8[6]);
+        g8[7] = fmaf(u, v1.w, g8[7]);
+        g3[0] = fmaf(p, qq.x, g3[0]);
+        g3[1] = fmaf(p, qq.y, g3[1]);
+        g3[2] = fmaf(p, qq.z, g3[2]);
+        gp += p;
+        gu += u;
+        gq[0] += qq.x;
+        gq[1] += qq.y;
+        gq[2] += qq.z;
+      }
+      // fold into the warp's partial row; every canonical entry has one owner lane
+      {
+        const int o = o16;
+        if (o < H) {
+          if (!hi_half) {
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              if (k < H) pw[2 * H + o * H + k] += g8[k];
+            pw[2 * o] += g3[0];
+            pw[2 * o + 1] += g3[1];
+            pw[L::P + o] += gp;      // b0
+            pw[L::P + H + o] += gu;  // b1
+          } else {
+#pragma unroll
+            for (int k = 0; k < 8; ++k)
+              if (8 + k < H) pw[2 * H + o * H + 8 + k] += g8[k];
+#pragma unroll
+            for (int j = 0; j < 3; ++j) pw[2 * H + H * H + j * H + o] += g3[j];
+            if (o == 0)
+#pragma unroll
+              for (int j = 0; j < 3; ++j) pw[L::P + 2 * H + j] += gq[j];
+          }
+        }
+      }
+      __syncwarp();
+    }
+    // loss of this step (weights before the update)
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) lp += __shfl_xor_sync(0xffffffffu, lp, d);
+    if (lane == 0) lossw[warp] = lp;
+    __syncthreads();
+    double loss = 0.0;
+    for (int i = 0; i < kFitWarps; ++i) loss += lossw[i];
+    loss *= scale;
+    if (!isfinite(loss)) {
+      status = t + 1;
+      break;
+    }
+    if (tid == 0 && (t % stride == 0 || t == A.steps) && slot_c < A.cap) A.curve[m * A.cap + slot_c++] = loss;
+    if (t == 0 && A.grad_w && !last) {
+      for (int p = tid; p < L::NPAR; p += kFitThreads) {
+        float g = 0.0f;
+        for (int i = 0; i < kFitWarps; ++i) g += part[i * L::NPAR_PAD + p];
+        if (p < L::P) A.grad_w[m * L::P + p] = __fmul_rn(g, mk[p]);
+        else A.grad_b[m * L::PB + p - L::P] = g;
+      }
+      if (tid == 0) A.loss0[m] = loss;
+      if (A.steps == 0) break;
+    }
+    if (t == A.steps) break;
+    // Adam step (net.py:282-296), numpy's f32 operation order
+    const double c1d = 1.0 - pow(0.9, double(t + 1)), c2d = 1.0 - pow(0.999, double(t + 1));
+    const float c1 = float(c1d), c2 = float(c2d);
+    const float lr = float(0.5 * A.lr0 * (1.0 + cos(3.141592653589793 * double(t) / double(A.steps))));
+    for (int p = tid; p < L::NPAR; p += kFitThreads) {
+      float g = 0.0f;
+      for (int i = 0; i < kFitWarps; ++i) g += part[i * L::NPAR_PAD + p];
+      if (p < L::P) g = __fmul_rn(g, mk[p]);  // gw * mask
+      float mp = __fadd_rn(__fmul_rn(mo[p], 0.9f), __fmul_rn(float(1.0 - 0.9), g));
+      float vp = __fadd_rn(__fmul_rn(ve[p], 0.999f), __fmul_rn(__fmul_rn(float(1.0 - 0.999), g), g));
+      mo[p] = mp;
+      ve[p] = vp;
+      const int s = L::slot(p);
+      const float upd = __fdiv_rn(__fmul_rn(lr, __fdiv_rn(mp, c1)), __fadd_rn(__fsqrt_rn(__fdiv_rn(vp, c2)), 1e-8f));
+      float w = __fsub_rn(ws[s], upd);
+      if (p < L::P) w = __fmul_rn(w, mk[p]);  // np.multiply(layer.w, mask)
+      ws[s] = w;
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  for (int p = tid; p < L::NPAR; p += kFitThreads) {
+    const float v = ws[L::slot(p)];
+    if (p < L::P) gw[p] = v;
+    else gb[p - L::P] = v;
+  }
+  if (tid == 0) {
+    A.status[m] = status;
+    for (int s = slot_c; s < A.cap; ++s) A.curve[m * A.cap + s] = NAN;
+  }
+}
+
+template <int H, bool ACC>
+__global__ void __launch_bounds__(256) render_kernel(int64_t n, const float* __restrict__ w,
+                                                     const float* __restrict__ b, int h, int wd, double inv_wm1,
+                                                     double inv_hm1, float om, float* __restrict__ out) {
+  using L = FitLayout<H>;
+  __shared__ __align__(16) float ws[L::WS];
+  const int64_t m = blockIdx.y;
+  for (int i = threadIdx.x; i < L::WS; i += 256) ws[i] = 0.0f;
+  __syncthreads();
+  for (int p = threadIdx.x; p < L::NPAR; p += 256) ws[L::slot(p)] = p < L::P ? w[m * L::P + p] : b[m * L::PB + p - L::P];
+  __syncthreads();
+  const int HW = h * wd;
+  const int px = blockIdx.x * 256 + threadIdx.x;
+  if (px >= HW) return;
+  const int pr = px / wd, pc = px - pr * wd;
+  const float x = grid_coord(pc, wd, inv_wm1), y = grid_coord(pr, h, inv_hm1);
+  float a0[16], c0[16], a1[16], c1[16], d2[3], o[3];
+  double lp = 0.0;
+  pixel_pass<H, ACC, false>(ws, x, y, nullptr, om, 0.0f, a0, c0, a1, c1, d2, o, lp);
+  float* dst = out + (m * HW + px) * 3;
+#pragma unroll
+  for (int j = 0; j < 3; ++j) dst[j] = fminf(fmaxf(o[j], 0.0f), 1.0f);  // np.clip(rgb, 0, 1)
+}
+
+int fit_arch(const int32_t* dims, int nl, int& H) {
+  if (!dims || nl != 3 || dims[0] != 2 || dims[3] != 3 || dims[1] != dims[2] || dims[1] < 8 || dims[1] > 16)
+    return set_error(RINR_ERR_UNSUPPORTED, "the GPU encoder supports architectures (2, H, H, 3) with 8 <= H <= 16");
+  H = dims[1];
+  return RINR_OK;
+}
+
+template <int H, bool ACC>
+int launch_fit(const FitArgs& a, cudaStream_t st) {
+  constexpr size_t smem = FitLayout<H>::smem_bytes();
+  static_assert(smem <= 227 * 1024, "fit kernel shared memory");
+  static bool attr = false;
+  if (!attr) {
+    if (cudaFuncSetAttribute(fit_kernel<H, ACC>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) !=
+        cudaSuccess)
+      return set_error(RINR_ERR_CUDA, "fit smem attribute");
+    attr = true;
+  }
+  fit_kernel<H, ACC><<<unsigned(a.n), kFitThreads, smem, st>>>(a);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(RINR_ERR_CUDA, std::string("fit launch: ") + cudaGetErrorString(e));
+  return RINR_OK;
+}
+
+template <int H>
+int dispatch_fit(const FitArgs& a, bool acc, cudaStream_t st) {
+  return acc ? launch_fit<H, true>(a, st) : launch_fit<H, false>(a, st);
+}
+
+template <int H, bool ACC>
+int launch_render(int64_t n, const float* w, const float* b, int h, int wd, double om, float* out, cudaStream_t st) {
+  const dim3 grid(unsigned((h * wd + 255) / 256), unsigned(n));
+  render_kernel<H, ACC><<<grid, 256, 0, st>>>(n, w, b, h, wd, wd > 1 ? 1.0 / double(wd - 1) : 0.0,
+                                              h > 1 ? 1.0 / double(h - 1) : 0.0, float(om), out);
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(RINR_ERR_CUDA, std::string("render launch: ") + cudaGetErrorString(e));
+  return RINR_OK;
+}
+
+}  // namespace
+}  // namespace rinr
+
+using namespace rinr;
+
+extern "C" int rinr_fit(const int32_t* dims, int nl, int64_t n, float* d_w, float* d_b, const uint8_t* d_mask,
+                        const float* d_images, const rinr_fit_params_t* p, double* d_curve, int32_t* d_status,
+                        float* d_grad_w, float* d_grad_b, double* d_loss0, void* stream) {
+  clear_error();
+  int H = 0;
+  if (int e = fit_arch(dims, nl, H)) return e;
+  if (!p || n < 0) return set_error(RINR_ERR_INVALID_INPUT, "null params or negative n");
+  if (p->h < 1 || p->w < 1 || p->steps < 0 || p->curve_cap < 1) return set_error(RINR_ERR_INVALID_INPUT, "bad fit params");
+  if (n == 0) return RINR_OK;
+  if (!d_w || !d_b || !d_mask || !d_images || !d_curve || !d_status)
+    return set_error(RINR_ERR_INVALID_INPUT, "null buffer");
+  if ((d_grad_w == nullptr) != (d_grad_b == nullptr) || (d_grad_w && !d_loss0))
+    return set_error(RINR_ERR_INVALID_INPUT, "grad outputs need d_grad_w, d_grad_b and d_loss0");
+  FitArgs a{};
+  a.n = n;
+  a.w = d_w;
+  a.b = d_b;
+  a.mask = d_mask;
+  a.images = d_images;
+  a.h = p->h;
+  a.wd = p->w;
+  a.hw = p->h * p->w;
+  a.steps = p->steps;
+  a.cap = p->curve_cap;
+  a.inv_wm1 = p->w > 1 ? 1.0 / double(p->w - 1) : 0.0;
+  a.inv_hm1 = p->h > 1 ? 1.0 / double(p->h - 1) : 0.0;
+  a.lr0 = p->lr0;
+  a.omega = p->omega;
+  a.curve = d_curve;
+  a.status = d_status;
+  a.grad_w = d_grad_w;
+  a.grad_b = d_grad_b;
+  a.loss0 = d_loss0;
+  const bool acc = p->sin_mode == RINR_SIN_ACCURATE;
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  switch (H) {
+    case 8: return dispatch_fit<8>(a, acc, st);
+    case 15: return dispatch_fit<15>(a, acc, st);
+    case 16: return dispatch_fit<16>(a, acc, st);
+    default: return set_error(RINR_ERR_UNSUPPORTED, "GPU encoder built for H in {8, 15, 16}");
+  }
+}
+
+extern "C" int rinr_fit_render(const int32_t* dims, int nl, int64_t n, const float* d_w, const float* d_b, int32_t h,
+                               int32_t w, double omega, int32_t sin_mode, float* d_out, void* stream) {
+  clear_error();
+  int H = 0;
+  if (int e = fit_arch(dims, nl, H)) return e;
+  if (n < 0 || h < 1 || w < 1) return set_error(RINR_ERR_INVALID_INPUT, "bad render size");
+  if (n == 0) return RINR_OK;
+  if (!d_w || !d_b || !d_out) return set_error(RINR_ERR_INVALID_INPUT, "null buffer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const bool acc = sin_mode == RINR_SIN_ACCURATE;
+  switch (H) {
+    case 8: return acc ? launch_render<8, true>(n, d_w, d_b, h, w, omega, d_out, st)
+                       : launch_render<8, false>(n, d_w, d_b, h, w, omega, d_out, st);
+    case 15: return acc ? launch_render<15, true>(n, d_w, d_b, h, w, omega, d_out, st)
+                        : launch_render<15, false>(n, d_w, d_b, h, w, omega, d_out, st);
+    case 16: return acc ? launch_render<16, true>(n, d_w, d_b, h, w, omega, d_out, st)
+                        : launch_render<16, false>(n, d_w, d_b, h, w, omega, d_out, st);
+    default: return set_error(RINR_ERR_UNSUPPORTED, "GPU encoder built for H in {8, 15, 16}");
+  }
+}

@@ -238,6 +238,71 @@ def transforms_case():
     np.savez_compressed(OUT / "transforms.npz", **out)
 
 
+def test_images(n, h, w, seed):
+    """Smooth deterministic RGB test images in [0, 1] (f32)."""
+    rng = np.random.default_rng(seed)
+    yy, xx = np.meshgrid(np.linspace(0, 1, h), np.linspace(0, 1, w), indexing="ij")
+    out = []
+    for _ in range(n):
+        img = np.zeros((h, w, 3), np.float64)
+        for c in range(3):
+            for _ in range(3):
+                fx, fy, ph = rng.uniform(0.5, 4.0), rng.uniform(0.5, 4.0), rng.uniform(0, 2 * np.pi)
+                img[..., c] += rng.uniform(0.1, 0.3) * np.sin(2 * np.pi * (fx * xx + fy * yy) + ph)
+        out.append(np.clip(0.5 + img, 0.0, 1.0).astype(np.float32))
+    return np.stack(out)
+
+
+def encoder_case():
+    """net.loss_and_grad / Adam / encoder._train / fit_round1 / fit_full pinned
+    by the reference (checker for the GPU encoder)."""
+    from rinr import encoder
+    from rinr.image import ImageBuffer
+    out = {}
+    imgs = test_images(3, 16, 16, seed=21)
+    out["images16"] = imgs
+    coords = net.coordinate_grid(16, 16)
+    # (1) loss + gradients: fresh init, and a pruned + perturbed model
+    for k, seed in enumerate((31, 32)):
+        m = net.init(ARCH_A, seed)
+        if k == 1:
+            m = compressor.prune_l1(m, 0.3)
+            for l in m.layers:
+                l.b[:] = np.random.default_rng(seed).normal(0, 0.05, l.b.shape).astype(np.float32)
+        loss, grads = net.loss_and_grad(m, coords, imgs[k].reshape(-1, 3))
+        out[f"grad{k}/seed"] = np.int64(seed)
+        out[f"grad{k}/w"] = np.concatenate([l.w.ravel() for l in m.layers])
+        out[f"grad{k}/b"] = np.concatenate([l.b.ravel() for l in m.layers])
+        out[f"grad{k}/mask"] = np.concatenate([x.ravel() for x in m.mask]).astype(np.uint8)
+        out[f"grad{k}/loss"] = np.float64(loss)
+        out[f"grad{k}/gw"] = np.concatenate([g.w.ravel() for g in grads])
+        out[f"grad{k}/gb"] = np.concatenate([g.b.ravel() for g in grads])
+    # (2) _train: 40 steps from init on image 2
+    m = net.init(ARCH_A, 33)
+    curve = []
+    encoder._train(m, coords, imgs[2].reshape(-1, 3), 5e-4, 40, curve)
+    out["train/curve"] = np.array(curve)
+    out["train/w"] = np.concatenate([l.w.ravel() for l in m.layers])
+    out["train/b"] = np.concatenate([l.b.ravel() for l in m.layers])
+    # (3) fit_round1 / fit_full on 32x32 images with shortened schedules
+    imgs32 = test_images(2, 32, 32, seed=22)
+    out["images32"] = imgs32
+    cfg1 = encoder.EncodeConfig(ARCH_A, round1_steps=300, seed=encoder.derive_seed(7, 0))
+    m1, r1_ = encoder.fit_round1(ImageBuffer(imgs32[0]), cfg1)
+    out["round1/seed"] = np.int64(cfg1.seed)
+    out["round1/psnr"] = np.array(r1_.psnr_after_round)
+    out["round1/curve"] = np.array(r1_.loss_curve)
+    cfgf = encoder.EncodeConfig(ARCH_A, round1_steps=200, retrain_steps=100, seed=encoder.derive_seed(7, 1))
+    mf, rf = encoder.fit_full(ImageBuffer(imgs32[1]), cfgf)
+    out["full/seed"] = np.int64(cfgf.seed)
+    out["full/psnr"] = np.array(rf.psnr_after_round)
+    out["full/psnr_mask"] = np.array(rf.psnr_after_mask)
+    out["full/ratio"] = np.float64(rf.final_prune_ratio)
+    out["derive_seed"] = np.array([encoder.derive_seed(s, i) for s in (0, 7, 2**40) for i in (0, 1, 999)],
+                                  np.uint64)
+    np.savez_compressed(OUT / "encoder.npz", **out)
+
+
 def _src(m, h=32, w=32):
     m.source_h, m.source_w = h, w
     return m
@@ -245,6 +310,9 @@ def _src(m, h=32, w=32):
 
 if __name__ == "__main__" and sys.argv[1:] == ["transforms"]:
     transforms_case()
+elif __name__ == "__main__" and sys.argv[1:] == ["encoder"]:
+    encoder_case()
 elif __name__ == "__main__":
     main()
     transforms_case()
+    encoder_case()

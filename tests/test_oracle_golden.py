@@ -125,3 +125,30 @@ def test_transforms_oracle(golden):
     for k in range(a.shape[0]):
         assert O.psnr(a[k], b2[k]) == g["psnr/f"][k]
         assert O.psnr(a[k], b2[k], quantized=True) == g["psnr/q"][k]
+
+
+# ---- training (net.py:152-300, encoder.py:28-85) --------------------------------
+
+def test_training_oracle(golden):
+    from transforms_common import split, split_bias
+    g = golden("encoder")
+    dims = (2, 15, 15, 3)
+    coords = O.coordinate_grid(16, 16)
+    imgs = g["images16"]
+    for k in (0, 1):
+        ws = split(g[f"grad{k}/w"], dims)
+        bs = split_bias(g[f"grad{k}/b"], dims)
+        ms = split(g[f"grad{k}/mask"], dims, bool)
+        if k == 0:
+            iw, ib, im = O.init_model(dims, int(g[f"grad{k}/seed"]))
+            for a, b in zip(iw, ws):
+                np.testing.assert_array_equal(a, b)
+        loss, gws, gbs = O.loss_and_grad(ws, bs, ms, 30.0, coords, imgs[k].reshape(-1, 3))
+        assert loss == g[f"grad{k}/loss"]
+        np.testing.assert_array_equal(np.concatenate([x.ravel() for x in gws]), g[f"grad{k}/gw"])
+        np.testing.assert_array_equal(np.concatenate([x.ravel() for x in gbs]), g[f"grad{k}/gb"])
+    ws, bs, ms = O.init_model(dims, 33)
+    curve = O.train(ws, bs, ms, 30.0, coords, imgs[2].reshape(-1, 3), 5e-4, 40)
+    np.testing.assert_array_equal(curve, g["train/curve"])
+    np.testing.assert_array_equal(np.concatenate([x.ravel() for x in ws]), g["train/w"])
+    np.testing.assert_array_equal(np.concatenate([x.ravel() for x in bs]), g["train/b"])
