@@ -324,8 +324,9 @@ int launch_tc_t(const StoreView& sv, const int64_t* ids, int64_t n, const Decode
   lay.tab_floats = ((a.out_w + 3) & ~3) + ((a.out_h + 3) & ~3);
   lay.rec_bytes = (sv.max_slot_bytes + 16 + 15) & ~15;
   lay.pfx_words = (NL * 2 * KW + 3) & ~3;
-  lay.tmem_cols = T * C::SLOT_COLS <= 128 ? 128 : (T * C::SLOT_COLS <= 256 ? 256 : 512);
-  static_assert(T * C::SLOT_COLS <= 512, "TMEM holds 512 columns");
+  constexpr int SLOT = C::slot_cols(X3);
+  lay.tmem_cols = T * SLOT <= 128 ? 128 : (T * SLOT <= 256 ? 256 : 512);
+  static_assert(T * SLOT <= 512, "TMEM holds 512 columns");
   const bool shared_tab = a.aug == RINR_AUG_NONE;
   const size_t budget = 227 * 1024;
   auto need = [&](int maxi, size_t& r0) {
@@ -368,8 +369,10 @@ int launch_tc_t(const StoreView& sv, const int64_t* ids, int64_t n, const Decode
 template <int HID, int NL, bool X3>
 int launch_tc(const StoreView& sv, const int64_t* ids, int64_t n, const DecodeArgs& a, const float* aug, void* out,
               int32_t* status, cudaStream_t st, float omega, int flags) {
-  if (sv.hidden_int8) return launch_tc_t<HID, NL, X3, 4, true>(sv, ids, n, a, aug, out, status, st, omega, flags);
-  return launch_tc_t<HID, NL, X3, 4, false>(sv, ids, n, a, aug, out, status, st, omega, flags);
+  // bf16 slots are 96 TMEM columns: 5 in flight (20 warps); X3 slots 128: 4
+  constexpr int T = X3 ? 4 : 5;
+  if (sv.hidden_int8) return launch_tc_t<HID, NL, X3, T, true>(sv, ids, n, a, aug, out, status, st, omega, flags);
+  return launch_tc_t<HID, NL, X3, T, false>(sv, ids, n, a, aug, out, status, st, omega, flags);
 }
 
 template <int HID, int NL, bool X3, bool ACC>

@@ -138,7 +138,9 @@ struct TcCfg {
   static constexpr int BHL_BYTES = INTB ? 0 : BH_BYTES;
   static constexpr int NET_BYTES = NH * (BH_BYTES + BHL_BYTES) + BO_BYTES * 2 + KP * 16 + NH * KP * 4 + 16 * 4 + NH * 8;
   // TMEM columns per tile slot: D (NP f32) at +0, A hi at +64, A lo at +96
+  // (X3); bf16 mode has no A lo, so its slots are 96 columns and 5 fit.
   static constexpr int SLOT_COLS = 128;
+  static constexpr int slot_cols(bool x3) { return x3 ? 128 : 96; }
 };
 
 // Per-image network view (K-major B matrices + scalars).
@@ -391,10 +393,11 @@ __global__ void __launch_bounds__(4 * T * 32, 1)
       const int s = warp >> 2;          // tile slot
       const int q = warp & 3;           // TMEM lane quarter
       const int row = q * 32 + lane;    // pixel row within the tile
-      const uint32_t tacc = tmem_base + uint32_t(s * C::SLOT_COLS) + (uint32_t(q * 32) << 16);
+      constexpr int SLOT = C::slot_cols(X3);
+      const uint32_t tacc = tmem_base + uint32_t(s * SLOT) + (uint32_t(q * 32) << 16);
       const uint32_t tahi = tacc + 64, talo = tacc + 96;
       const bool issuer = q == 0 && lane == 0;
-      const uint32_t dslot = tmem_base + uint32_t(s * C::SLOT_COLS);
+      const uint32_t dslot = tmem_base + uint32_t(s * SLOT);
       const float invW = 1.0f / float(a.out_w);
       for (int r = 0; r < rounds; ++r) {
         const int t = ts + r * T + s;
