@@ -370,7 +370,7 @@ template <int HID, int NL, bool X3>
 int launch_tc(const StoreView& sv, const int64_t* ids, int64_t n, const DecodeArgs& a, const float* aug, void* out,
               int32_t* status, cudaStream_t st, float omega, int flags) {
   // bf16 slots are 96 TMEM columns: 5 in flight (20 warps); X3 slots 128: 4
-  constexpr int T = X3 ? 4 : 5;
+  constexpr int T = X3 ? 5 : 6;
   if (sv.hidden_int8) return launch_tc_t<HID, NL, X3, T, true>(sv, ids, n, a, aug, out, status, st, omega, flags);
   return launch_tc_t<HID, NL, X3, T, false>(sv, ids, n, a, aug, out, status, st, omega, flags);
 }

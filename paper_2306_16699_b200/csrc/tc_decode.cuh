@@ -140,7 +140,10 @@ struct TcCfg {
   // TMEM columns per tile slot: D (NP f32) at +0, A hi at +64, A lo at +96
   // (X3); bf16 mode has no A lo, so its slots are 96 columns and 5 fit.
   static constexpr int SLOT_COLS = 128;
-  static constexpr int slot_cols(bool x3) { return x3 ? 128 : 96; }
+  // packed: D (NP f32 columns) | A hi (KP/2) | A lo (KP/2, X3 only)
+  static constexpr int slot_cols(bool x3) { return (NP + (x3 ? KP : KP / 2) + 15) / 16 * 16; }
+  static constexpr int ahi_col(bool) { return NP; }
+  static constexpr int alo_col() { return NP + KP / 2; }
 };
 
 // Per-image network view (K-major B matrices + scalars).
@@ -205,7 +208,7 @@ __device__ __forceinline__ void issue_layer(const TcNet<HID, NL, INTB>& net, uin
   using C = TcCfg<HID, NL, INTB>;
   constexpr uint32_t IDESC_H = tc::make_idesc(128, C::NP);
   constexpr uint32_t IDESC_O = tc::make_idesc(128, C::NO);
-  const uint32_t ahi = d + 64, alo = d + 96;
+  const uint32_t ahi = d + C::ahi_col(X3), alo = d + C::alo_col();
   const bool outl = l == NL - 2;
   const uint32_t bhi = tc::smem_u32(outl ? net.bo_hi : net.bh_hi + l * C::BH_BYTES);
   const uint32_t blo = tc::smem_u32(outl ? net.bo_lo : net.bh_lo + l * C::BH_BYTES);
@@ -395,7 +398,7 @@ __global__ void __launch_bounds__(4 * T * 32, 1)
       const int row = q * 32 + lane;    // pixel row within the tile
       constexpr int SLOT = C::slot_cols(X3);
       const uint32_t tacc = tmem_base + uint32_t(s * SLOT) + (uint32_t(q * 32) << 16);
-      const uint32_t tahi = tacc + 64, talo = tacc + 96;
+      const uint32_t tahi = tacc + C::ahi_col(X3), talo = tacc + C::alo_col();
       const bool issuer = q == 0 && lane == 0;
       const uint32_t dslot = tmem_base + uint32_t(s * SLOT);
       const float invW = 1.0f / float(a.out_w);
