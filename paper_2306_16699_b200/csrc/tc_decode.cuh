@@ -425,10 +425,14 @@ __global__ void __launch_bounds__(4 * T * 32, 1)
           for (int half = 0; half < 2; ++half) {
             float v[8];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) {
+            for (int e = 0; e < 8; e += 2) {  // two columns per FFMA2 pair
               const int col = ks * 16 + half * 8 + e;
               const float4 w = reinterpret_cast<const float4*>(net.l0)[col];
-              v[e] = col < HID ? __sinf(fmaf(w.y, y, fmaf(w.x, x, w.z))) : 0.0f;
+              const float4 w2 = reinterpret_cast<const float4*>(net.l0)[col + 1];
+              const float2 z = ffma2(make_float2(w.y, w2.y), make_float2(y, y),
+                                     ffma2(make_float2(w.x, w2.x), make_float2(x, x), make_float2(w.z, w2.z)));
+              v[e] = col < HID ? __sinf(z.x) : 0.0f;
+              v[e + 1] = col + 1 < HID ? __sinf(z.y) : 0.0f;
             }
 #pragma unroll
             for (int i2 = 0; i2 < 4; ++i2) pack_act<X3>(v[2 * i2], v[2 * i2 + 1], hi[half * 4 + i2], lo[half * 4 + i2]);
@@ -465,8 +469,12 @@ __global__ void __launch_bounds__(4 * T * 32, 1)
                 const float4 b1 = reinterpret_cast<const float4*>(bias)[2 * cchunk + 1];
                 const float bb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
 #pragma unroll
-                for (int e = 0; e < 8; ++e)
-                  u[e] = cchunk * 8 + e < HID ? __sinf(fmaf(v[cchunk < CV ? cchunk : 0][e], sc, bb[e])) : 0.0f;
+                for (int e = 0; e < 8; e += 2) {  // packed scale + bias (FFMA2)
+                  const float* vc = v[cchunk < CV ? cchunk : 0];
+                  const float2 z = ffma2(make_float2(vc[e], vc[e + 1]), make_float2(sc, sc), make_float2(bb[e], bb[e + 1]));
+                  u[e] = cchunk * 8 + e < HID ? __sinf(z.x) : 0.0f;
+                  u[e + 1] = cchunk * 8 + e + 1 < HID ? __sinf(z.y) : 0.0f;
+                }
               } else {
 #pragma unroll
                 for (int e = 0; e < 8; ++e) u[e] = 0.0f;
