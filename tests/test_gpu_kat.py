@@ -73,3 +73,34 @@ def test_last_layer_linear(precision):
     # and against the oracle
     want = np.stack(O.decode_batch(O.read_models(_store_bytes(full)), 16, 16)).transpose(0, 3, 1, 2)
     assert float(np.abs(fa - want).max()) <= 1e-3
+
+
+@pytest.mark.parametrize("arch_name,precision", [("ARCH_A", "fp32"), ("ARCH_C", "bf16"), ("ARCH_C", "fp32"),
+                                                 ("ZOO", "exact")])
+def test_large_output_sampled(arch_name, precision):
+    """Maximum-size path: 2048 x 2048 decodes on every kernel family, checked
+    against the oracle's forward on sampled pixels (rows/cols at the edges
+    and the middle)."""
+    from paper_2306_16699_b200 import Store, synth
+    if arch_name == "ZOO":
+        mb = synth.tweak_r1(synth.seeded_batch(synth.Architecture((2, 7, 11, 3)), range(2)))
+    else:
+        mb = synth.tweak_r1(synth.seeded_batch(getattr(synth, arch_name), range(2)))
+    data = synth.archive_bytes(mb)
+    models = O.read_models(data)
+    H = W = 2048
+    with Store(data) as st:
+        out = st.decode(torch.arange(2), H, W, layout="nhwc", precision=precision).cpu().numpy()
+    assert np.isfinite(out).all() and out.min() >= 0.0 and out.max() <= 1.0
+    xs = O.axis_coords(W)
+    rows = [0, 1, 1023, 2046, 2047]
+    cols = np.array([0, 1, 777, 1024, 2046, 2047])
+    for i, m in enumerate(models):
+        for r in rows:
+            c = np.stack([xs[cols], np.full(len(cols), O.axis_coords(H)[r], np.float32)], 1)
+            want = np.clip(O.forward(m, c), 0.0, 1.0)
+            got = out[i, r, cols]
+            if precision == "bf16":
+                assert float(np.abs(got - want).max()) <= 2e-2
+            else:
+                assert float(np.abs(got - want).max()) <= 1e-3
