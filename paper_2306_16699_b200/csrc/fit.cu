@@ -19,6 +19,7 @@
 
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <string>
 
 #include "../../include/rinr_b200_encoder.h"
@@ -56,9 +57,9 @@ struct FitLayout {
     if (p < H) return B1S + p;
     return B2S + (p - H);
   }
-  static constexpr size_t smem_bytes() {
-    return sizeof(float) * (size_t(WS) + 2 * NPAR_PAD + ((P + 3) & ~3) + size_t(kFitWarps) * NPAR_PAD +
-                            size_t(kFitWarps) * 32 * kStage) +
+  static constexpr size_t smem_bytes(int npx) {
+    return sizeof(float) * (size_t(WS) + 2 * NPAR_PAD + ((P + 3) & ~3) + size_t(kFitWarps / npx) * NPAR_PAD +
+                            size_t(kFitWarps / npx) * 32 * npx * kStage) +
            sizeof(double) * kFitWarps;
   }
 };
@@ -111,12 +112,14 @@ __device__ __forceinline__ void wrow(const float* p, float (&r)[16]) {
   }
 }
 
-// Per-pixel forward (+ backward when BWD): a0/c0/a1/c1 (c = omega cos(omega z));
-// on return of the backward, c1 holds d1 and c0 holds d0.
-template <int H, bool ACC, bool BWD>
-__device__ __forceinline__ void pixel_pass(const float* __restrict__ ws, float x, float y, const float* tg, float om,
-                                           float s2, float (&a0)[16], float (&c0)[16], float (&a1)[16],
-                                           float (&c1)[16], float (&d2)[3], float (&out)[3], double& lp) {
+// Forward (+ backward when BWD) of NPX pixels per thread: a0/c0/a1/c1
+// (c = omega cos(omega z)); on return of the backward, c1 holds d1 and c0
+// holds d0.  Every weight row loaded from shared memory serves all NPX pixels.
+template <int H, bool ACC, bool BWD, int NPX>
+__device__ __forceinline__ void pixel_pass(const float* __restrict__ ws, const float (&x)[NPX], const float (&y)[NPX],
+                                           const float (&tg)[NPX][3], float om, float s2, float (&a0)[NPX][16],
+                                           float (&c0)[NPX][16], float (&a1)[NPX][16], float (&c1)[NPX][16],
+                                           float (&d2)[NPX][3], float (&out)[NPX][3], double (&lp)[NPX]) {
   using L = FitLayout<H>;
   float r[16], bb[16];
   // layer 0: 2 -> H (W0 rows are float2 pairs: 8 rows per 4 loads)
@@ -129,11 +132,14 @@ __device__ __forceinline__ void pixel_pass(const float* __restrict__ ws, float x
       const int o = o0 + h;
       if (o < H) {
         const float wx = h ? w.z : w.x, wy = h ? w.w : w.y;
-        const float z = __fadd_rn(fmaf(y, wy, __fmul_rn(x, wx)), bb[o]);
-        float s, c;
-        sincos_<ACC>(__fmul_rn(om, z), s, c);
-        a0[o] = s;
-        c0[o] = __fmul_rn(om, c);
+#pragma unroll
+        for (int p = 0; p < NPX; ++p) {
+          const float z = __fadd_rn(fmaf(y[p], wy, __fmul_rn(x[p], wx)), bb[o]);
+          float s, c;
+          sincos_<ACC>(__fmul_rn(om, z), s, c);
+          a0[p][o] = s;
+          c0[p][o] = __fmul_rn(om, c);
+        }
       }
     }
   }
@@ -142,77 +148,100 @@ __device__ __forceinline__ void pixel_pass(const float* __restrict__ ws, float x
 #pragma unroll
   for (int o = 0; o < H; ++o) {
     wrow<H>(ws + L::W1S + 16 * o, r);
-    float acc = 0.0f;
 #pragma unroll
-    for (int k = 0; k < H; ++k) acc = fmaf(a0[k], r[k], acc);
-    float s, c;
-    sincos_<ACC>(__fmul_rn(om, __fadd_rn(acc, bb[o])), s, c);
-    a1[o] = s;
-    c1[o] = __fmul_rn(om, c);
+    for (int p = 0; p < NPX; ++p) {
+      float acc = 0.0f;
+#pragma unroll
+      for (int k = 0; k < H; ++k) acc = fmaf(a0[p][k], r[k], acc);
+      float s, c;
+      sincos_<ACC>(__fmul_rn(om, __fadd_rn(acc, bb[o])), s, c);
+      a1[p][o] = s;
+      c1[p][o] = __fmul_rn(om, c);
+    }
   }
   // layer 2: H -> 3 (affine)
   const float4 b2 = wld4(ws + L::B2S);
 #pragma unroll
   for (int j = 0; j < 3; ++j) {
     wrow<H>(ws + L::W2S + 16 * j, r);
-    float acc = 0.0f;
 #pragma unroll
-    for (int k = 0; k < H; ++k) acc = fmaf(a1[k], r[k], acc);
-    out[j] = __fadd_rn(acc, j == 0 ? b2.x : (j == 1 ? b2.y : b2.z));
+    for (int p = 0; p < NPX; ++p) {
+      float acc = 0.0f;
+#pragma unroll
+      for (int k = 0; k < H; ++k) acc = fmaf(a1[p][k], r[k], acc);
+      out[p][j] = __fadd_rn(acc, j == 0 ? b2.x : (j == 1 ? b2.y : b2.z));
+    }
   }
   if constexpr (BWD) {
 #pragma unroll
-    for (int j = 0; j < 3; ++j) {
-      const float e = __fsub_rn(out[j], tg[j]);
-      lp += double(e) * double(e);
-      d2[j] = __fmul_rn(s2, e);  // (2.0 * scale) * resid
-    }
+    for (int p = 0; p < NPX; ++p)
+#pragma unroll
+      for (int j = 0; j < 3; ++j) {
+        const float e = __fsub_rn(out[p][j], tg[p][j]);
+        lp[p] += double(e) * double(e);
+        d2[p][j] = __fmul_rn(s2, e);  // (2.0 * scale) * resid
+      }
     // d1 = (d2 @ W2) * c1
-    float g[16];
+    float g[NPX][16];
     wrow<H>(ws + L::W2S, r);
 #pragma unroll
-    for (int k = 0; k < H; ++k) g[k] = __fmul_rn(d2[0], r[k]);
+    for (int p = 0; p < NPX; ++p)
+#pragma unroll
+      for (int k = 0; k < H; ++k) g[p][k] = __fmul_rn(d2[p][0], r[k]);
 #pragma unroll
     for (int j = 1; j < 3; ++j) {
       wrow<H>(ws + L::W2S + 16 * j, r);
 #pragma unroll
-      for (int k = 0; k < H; ++k) g[k] = fmaf(d2[j], r[k], g[k]);
+      for (int p = 0; p < NPX; ++p)
+#pragma unroll
+        for (int k = 0; k < H; ++k) g[p][k] = fmaf(d2[p][j], r[k], g[p][k]);
     }
 #pragma unroll
-    for (int k = 0; k < H; ++k) c1[k] = __fmul_rn(g[k], c1[k]);
+    for (int p = 0; p < NPX; ++p)
+#pragma unroll
+      for (int k = 0; k < H; ++k) c1[p][k] = __fmul_rn(g[p][k], c1[p][k]);
     // d0 = (d1 @ W1) * c0, row-outer so each W1 row is 4 vector loads
 #pragma unroll
-    for (int k = 0; k < H; ++k) g[k] = 0.0f;
+    for (int p = 0; p < NPX; ++p)
+#pragma unroll
+      for (int k = 0; k < H; ++k) g[p][k] = 0.0f;
 #pragma unroll
     for (int o = 0; o < H; ++o) {
       wrow<H>(ws + L::W1S + 16 * o, r);
 #pragma unroll
-      for (int k = 0; k < H; ++k) g[k] = fmaf(c1[o], r[k], g[k]);
+      for (int p = 0; p < NPX; ++p)
+#pragma unroll
+        for (int k = 0; k < H; ++k) g[p][k] = fmaf(c1[p][o], r[k], g[p][k]);
     }
 #pragma unroll
-    for (int k = 0; k < H; ++k) c0[k] = __fmul_rn(g[k], c0[k]);
+    for (int p = 0; p < NPX; ++p)
+#pragma unroll
+      for (int k = 0; k < H; ++k) c0[p][k] = __fmul_rn(g[p][k], c0[p][k]);
   }
 }
 
-template <int H, bool ACC>
-__global__ void __launch_bounds__(kFitThreads, 1) fit_kernel(FitArgs A) {
+template <int H, bool ACC, int NPX>
+__global__ void __launch_bounds__(kFitThreads / NPX, 1) fit_kernel(FitArgs A) {
   using L = FitLayout<H>;
+  constexpr int NWP = kFitWarps / NPX;         // warps per CTA
+  constexpr int NTH = NWP * 32;                // threads per CTA
+  constexpr int CPX = 32 * NPX;                // pixels per warp chunk
   extern __shared__ __align__(16) float sm[];
   float* ws = sm;
   float* mo = ws + L::WS;
   float* ve = mo + L::NPAR_PAD;
   float* mk = ve + L::NPAR_PAD;
   float* part = mk + ((L::P + 3) & ~3);
-  float* stage = part + kFitWarps * L::NPAR_PAD;
-  double* lossw = reinterpret_cast<double*>(stage + kFitWarps * 32 * kStage);
+  float* stage = part + NWP * L::NPAR_PAD;
+  double* lossw = reinterpret_cast<double*>(stage + NWP * CPX * kStage);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t m = blockIdx.x;
   float* gw = A.w + m * L::P;
   float* gb = A.b + m * L::PB;
 
-  for (int i = tid; i < L::WS; i += kFitThreads) ws[i] = 0.0f;
+  for (int i = tid; i < L::WS; i += NTH) ws[i] = 0.0f;
   __syncthreads();
-  for (int p = tid; p < L::NPAR; p += kFitThreads) {
+  for (int p = tid; p < L::NPAR; p += NTH) {
     ws[L::slot(p)] = p < L::P ? gw[p] : gb[p - L::P];
     mo[p] = 0.0f;
     ve[p] = 0.0f;
@@ -220,13 +249,13 @@ __global__ void __launch_bounds__(kFitThreads, 1) fit_kernel(FitArgs A) {
   }
   __syncthreads();
 
-  const int HW = A.hw, nchunks = (HW + 31) / 32;
+  const int HW = A.hw, nchunks = (HW + CPX - 1) / CPX;
   const double scale = 1.0 / (3.0 * double(HW));  // 1.0 / resid.size
   const float s2 = float(2.0 * scale);
   const float om = float(A.omega);
   const int stride = A.steps / 64 > 1 ? A.steps / 64 : 1;
   const float* img = A.images + m * int64_t(HW) * 3;
-  float* st = stage + warp * 32 * kStage;
+  float* st = stage + warp * CPX * kStage;
   const int o16 = lane & 15;
   const bool hi_half = lane >= 16;
   int slot_c = 0;
@@ -242,39 +271,52 @@ __global__ void __launch_bounds__(kFitThreads, 1) fit_kernel(FitArgs A) {
       for (int i = lane; i < L::NPAR_PAD; i += 32) pw[i] = 0.0f;
     __syncwarp();
     double lp = 0.0;
-    for (int ch = warp; ch < nchunks; ch += kFitWarps) {
-      const int px = ch * 32 + lane;
-      const bool valid = px < HW;
-      const int pr = valid ? px / A.wd : 0, pc = valid ? px - pr * A.wd : 0;
-      const float x = grid_coord(pc, A.wd, A.inv_wm1), y = grid_coord(pr, A.h, A.inv_hm1);
-      float tg[3] = {0.f, 0.f, 0.f};
-      if (valid) {
-        tg[0] = img[3 * px];
-        tg[1] = img[3 * px + 1];
-        tg[2] = img[3 * px + 2];
+    for (int ch = warp; ch < nchunks; ch += NWP) {
+      float x[NPX], y[NPX], tg[NPX][3];
+      bool valid[NPX];
+#pragma unroll
+      for (int p = 0; p < NPX; ++p) {
+        const int px = ch * CPX + p * 32 + lane;
+        valid[p] = px < HW;
+        const int pr = valid[p] ? px / A.wd : 0, pc = valid[p] ? px - pr * A.wd : 0;
+        x[p] = grid_coord(pc, A.wd, A.inv_wm1);
+        y[p] = grid_coord(pr, A.h, A.inv_hm1);
+        tg[p][0] = tg[p][1] = tg[p][2] = 0.0f;
+        if (valid[p]) {
+          tg[p][0] = img[3 * px];
+          tg[p][1] = img[3 * px + 1];
+          tg[p][2] = img[3 * px + 2];
+        }
       }
-      float a0[16], c0[16], a1[16], c1[16], d2[3], out[3];
-      double lpx = 0.0;
-      pixel_pass<H, ACC, true>(ws, x, y, tg, om, s2, a0, c0, a1, c1, d2, out, lpx);
-      if (valid) lp += lpx;
+      float a0[NPX][16], c0[NPX][16], a1[NPX][16], c1[NPX][16], d2[NPX][3], out[NPX][3];
+      double lpx[NPX];
+#pragma unroll
+      for (int p = 0; p < NPX; ++p) lpx[p] = 0.0;
+      pixel_pass<H, ACC, true, NPX>(ws, x, y, tg, om, s2, a0, c0, a1, c1, d2, out, lpx);
+#pragma unroll
+      for (int p = 0; p < NPX; ++p)
+        if (valid[p]) lp += lpx[p];
       if (last) continue;
-      if (!valid) {
 #pragma unroll
-        for (int k = 0; k < 16; ++k) c0[k] = c1[k] = 0.0f;
-        d2[0] = d2[1] = d2[2] = 0.0f;
-      }
-      float* row = st + lane * kStage;
+      for (int p = 0; p < NPX; ++p) {
+        if (!valid[p]) {
 #pragma unroll
-      for (int k = 0; k < 16; k += 4) {
-        *reinterpret_cast<float4*>(row + SA0 + k) = make_float4(a0[k], a0[k + 1], a0[k + 2], a0[k + 3]);
-        *reinterpret_cast<float4*>(row + SA1 + k) = make_float4(a1[k], a1[k + 1], a1[k + 2], a1[k + 3]);
-        *reinterpret_cast<float4*>(row + SD1 + k) = make_float4(c1[k], c1[k + 1], c1[k + 2], c1[k + 3]);
-        *reinterpret_cast<float4*>(row + SD0 + k) = make_float4(c0[k], c0[k + 1], c0[k + 2], c0[k + 3]);
+          for (int k = 0; k < 16; ++k) c0[p][k] = c1[p][k] = 0.0f;
+          d2[p][0] = d2[p][1] = d2[p][2] = 0.0f;
+        }
+        float* row = st + (p * 32 + lane) * kStage;
+#pragma unroll
+        for (int k = 0; k < 16; k += 4) {
+          *reinterpret_cast<float4*>(row + SA0 + k) = make_float4(a0[p][k], a0[p][k + 1], a0[p][k + 2], a0[p][k + 3]);
+          *reinterpret_cast<float4*>(row + SA1 + k) = make_float4(a1[p][k], a1[p][k + 1], a1[p][k + 2], a1[p][k + 3]);
+          *reinterpret_cast<float4*>(row + SD1 + k) = make_float4(c1[p][k], c1[p][k + 1], c1[p][k + 2], c1[p][k + 3]);
+          *reinterpret_cast<float4*>(row + SD0 + k) = make_float4(c0[p][k], c0[p][k + 1], c0[p][k + 2], c0[p][k + 3]);
+        }
+        *reinterpret_cast<float4*>(row + SD2) = make_float4(d2[p][0], d2[p][1], d2[p][2], 0.0f);
+        *reinterpret_cast<float4*>(row + SXY) = make_float4(x[p], y[p], 0.0f, 0.0f);
       }
-      *reinterpret_cast<float4*>(row + SD2) = make_float4(d2[0], d2[1], d2[2], 0.0f);
-      *reinterpret_cast<float4*>(row + SXY) = make_float4(x, y, 0.0f, 0.0f);
       __syncwarp();
-      const int nq = HW - ch * 32 < 32 ? HW - ch * 32 : 32;
+      const int nq = HW - ch * CPX < CPX ? HW - ch * CPX : CPX;
       // per-lane accumulators live only for this chunk (uniform stream, see header)
       float g8[8], g3[3], gq[3], gp = 0.0f, gu = 0.0f;
 #pragma unroll
@@ -342,7 +384,7 @@ __global__ void __launch_bounds__(kFitThreads, 1) fit_kernel(FitArgs A) {
     if (lane == 0) lossw[warp] = lp;
     __syncthreads();
     double loss = 0.0;
-    for (int i = 0; i < kFitWarps; ++i) loss += lossw[i];
+    for (int i = 0; i < NWP; ++i) loss += lossw[i];
     loss *= scale;
     if (!isfinite(loss)) {
       status = t + 1;
@@ -350,9 +392,9 @@ __global__ void __launch_bounds__(kFitThreads, 1) fit_kernel(FitArgs A) {
     }
     if (tid == 0 && (t % stride == 0 || t == A.steps) && slot_c < A.cap) A.curve[m * A.cap + slot_c++] = loss;
     if (t == 0 && A.grad_w && !last) {
-      for (int p = tid; p < L::NPAR; p += kFitThreads) {
+      for (int p = tid; p < L::NPAR; p += NTH) {
         float g = 0.0f;
-        for (int i = 0; i < kFitWarps; ++i) g += part[i * L::NPAR_PAD + p];
+        for (int i = 0; i < NWP; ++i) g += part[i * L::NPAR_PAD + p];
         if (p < L::P) A.grad_w[m * L::P + p] = __fmul_rn(g, mk[p]);
         else A.grad_b[m * L::PB + p - L::P] = g;
       }
@@ -364,9 +406,9 @@ __global__ void __launch_bounds__(kFitThreads, 1) fit_kernel(FitArgs A) {
     const double c1d = 1.0 - pow(0.9, double(t + 1)), c2d = 1.0 - pow(0.999, double(t + 1));
     const float c1 = float(c1d), c2 = float(c2d);
     const float lr = float(0.5 * A.lr0 * (1.0 + cos(3.141592653589793 * double(t) / double(A.steps))));
-    for (int p = tid; p < L::NPAR; p += kFitThreads) {
+    for (int p = tid; p < L::NPAR; p += NTH) {
       float g = 0.0f;
-      for (int i = 0; i < kFitWarps; ++i) g += part[i * L::NPAR_PAD + p];
+      for (int i = 0; i < NWP; ++i) g += part[i * L::NPAR_PAD + p];
       if (p < L::P) g = __fmul_rn(g, mk[p]);  // gw * mask
       float mp = __fadd_rn(__fmul_rn(mo[p], 0.9f), __fmul_rn(float(1.0 - 0.9), g));
       float vp = __fadd_rn(__fmul_rn(ve[p], 0.999f), __fmul_rn(__fmul_rn(float(1.0 - 0.999), g), g));
@@ -381,7 +423,7 @@ __global__ void __launch_bounds__(kFitThreads, 1) fit_kernel(FitArgs A) {
     __syncthreads();
   }
   __syncthreads();
-  for (int p = tid; p < L::NPAR; p += kFitThreads) {
+  for (int p = tid; p < L::NPAR; p += NTH) {
     const float v = ws[L::slot(p)];
     if (p < L::P) gw[p] = v;
     else gb[p - L::P] = v;
@@ -408,12 +450,13 @@ __global__ void __launch_bounds__(256) render_kernel(int64_t n, const float* __r
   if (px >= HW) return;
   const int pr = px / wd, pc = px - pr * wd;
   const float x = grid_coord(pc, wd, inv_wm1), y = grid_coord(pr, h, inv_hm1);
-  float a0[16], c0[16], a1[16], c1[16], d2[3], o[3];
-  double lp = 0.0;
-  pixel_pass<H, ACC, false>(ws, x, y, nullptr, om, 0.0f, a0, c0, a1, c1, d2, o, lp);
+  float a0[1][16], c0[1][16], a1[1][16], c1[1][16], d2[1][3], o[1][3], tg[1][3] = {{0.f, 0.f, 0.f}};
+  double lp[1] = {0.0};
+  const float xs[1] = {x}, ys[1] = {y};
+  pixel_pass<H, ACC, false, 1>(ws, xs, ys, tg, om, 0.0f, a0, c0, a1, c1, d2, o, lp);
   float* dst = out + (m * HW + px) * 3;
 #pragma unroll
-  for (int j = 0; j < 3; ++j) dst[j] = fminf(fmaxf(o[j], 0.0f), 1.0f);  // np.clip(rgb, 0, 1)
+  for (int j = 0; j < 3; ++j) dst[j] = fminf(fmaxf(o[0][j], 0.0f), 1.0f);  // np.clip(rgb, 0, 1)
 }
 
 int fit_arch(const int32_t* dims, int nl, int& H) {
@@ -423,26 +466,33 @@ int fit_arch(const int32_t* dims, int nl, int& H) {
   return RINR_OK;
 }
 
-template <int H, bool ACC>
+template <int H, bool ACC, int NPX>
 int launch_fit(const FitArgs& a, cudaStream_t st) {
-  constexpr size_t smem = FitLayout<H>::smem_bytes();
+  constexpr size_t smem = FitLayout<H>::smem_bytes(NPX);
   static_assert(smem <= 227 * 1024, "fit kernel shared memory");
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(fit_kernel<H, ACC>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) !=
+    if (cudaFuncSetAttribute(fit_kernel<H, ACC, NPX>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) !=
         cudaSuccess)
       return set_error(RINR_ERR_CUDA, "fit smem attribute");
     attr = true;
   }
-  fit_kernel<H, ACC><<<unsigned(a.n), kFitThreads, smem, st>>>(a);
+  fit_kernel<H, ACC, NPX><<<unsigned(a.n), kFitThreads / NPX, smem, st>>>(a);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(RINR_ERR_CUDA, std::string("fit launch: ") + cudaGetErrorString(e));
   return RINR_OK;
 }
 
+// two pixels per thread (8 warps): each weight row from shared memory
+// serves two pixels (RINR_FIT_NPX=1 selects one pixel per thread, 16 warps)
 template <int H>
 int dispatch_fit(const FitArgs& a, bool acc, cudaStream_t st) {
-  return acc ? launch_fit<H, true>(a, st) : launch_fit<H, false>(a, st);
+  static const int npx = [] {
+    const char* e = std::getenv("RINR_FIT_NPX");
+    return e && e[0] == '1' ? 1 : 2;
+  }();
+  if (npx == 1) return acc ? launch_fit<H, true, 1>(a, st) : launch_fit<H, false, 1>(a, st);
+  return acc ? launch_fit<H, true, 2>(a, st) : launch_fit<H, false, 2>(a, st);
 }
 
 template <int H, bool ACC>
