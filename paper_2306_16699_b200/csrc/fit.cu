@@ -220,6 +220,110 @@ __device__ __forceinline__ void pixel_pass(const float* __restrict__ ws, const f
   }
 }
 
+// mma.sync m16n8k8 tf32 (f32 accumulate).  Operands are f32 registers; the
+// tensor core reads their top 19 bits.
+__device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm("mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};\n"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// x = hi + lo with hi = x's tf32 value (what the tensor core reads) and lo
+// the exact remainder (itself read as tf32): 3-pass products are fp32-accurate.
+__device__ __forceinline__ void tf32_split(float x, uint32_t& hi, uint32_t& lo) {
+  const uint32_t u = __float_as_uint(x);
+  hi = u;
+  lo = __float_as_uint(__fsub_rn(x, __uint_as_float(u & 0xffffe000u)));
+}
+
+// Outer-product gradient sums of one staged chunk on tensor cores (H < 16):
+//   gW1 | gb1 = d1^T [a0 | 1],   gW2 | gb2 = d2^T [a1 | 1],   gW0 | gb0 = d0^T [x y 1]
+// as M16 x N x K(=pixels) GEMMs in 3xTF32 (hi*hi + hi*lo + lo*hi), then the
+// fragments are added to the warp's partial row (each entry has one owner lane).
+template <int H>
+__device__ __forceinline__ void tc_reduce(const float* st, int rows, float* pw, int lane) {
+  using L = FitLayout<H>;
+  const int g = lane >> 2, tq = lane & 3;
+  // one accumulator per 3xTF32 pass: 15 independent MMA chains per k-step
+  float c1[3][2][4] = {}, c2[3][2][4] = {}, c0[3][4] = {};
+  for (int kb = 0; kb < rows; kb += 8) {
+    const float* r0 = st + (kb + tq) * kStage;      // pixel kb + tq
+    const float* r1 = st + (kb + tq + 4) * kStage;  // pixel kb + tq + 4
+    // A operands (rows = output unit, K = pixel): d1^T, d0^T, d2^T
+    uint32_t a1h[4], a1l[4], a0h[4], a0l[4], a2h[4], a2l[4];
+    tf32_split(r0[SD1 + g], a1h[0], a1l[0]);
+    tf32_split(r0[SD1 + g + 8], a1h[1], a1l[1]);
+    tf32_split(r1[SD1 + g], a1h[2], a1l[2]);
+    tf32_split(r1[SD1 + g + 8], a1h[3], a1l[3]);
+    tf32_split(r0[SD0 + g], a0h[0], a0l[0]);
+    tf32_split(r0[SD0 + g + 8], a0h[1], a0l[1]);
+    tf32_split(r1[SD0 + g], a0h[2], a0l[2]);
+    tf32_split(r1[SD0 + g + 8], a0h[3], a0l[3]);
+    tf32_split(g < 3 ? r0[SD2 + (g & 3)] : 0.0f, a2h[0], a2l[0]);
+    a2h[1] = a2l[1] = 0u;
+    tf32_split(g < 3 ? r1[SD2 + (g & 3)] : 0.0f, a2h[2], a2l[2]);
+    a2h[3] = a2l[3] = 0u;
+    uint32_t b1h[2][2], b1l[2][2], b2h[2][2], b2l[2][2], b0h[2], b0l[2];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      tf32_split(r0[SA0 + 8 * j + g], b1h[j][0], b1l[j][0]);  // B = [a0 | 1]
+      tf32_split(r1[SA0 + 8 * j + g], b1h[j][1], b1l[j][1]);
+      tf32_split(r0[SA1 + 8 * j + g], b2h[j][0], b2l[j][0]);  // B = [a1 | 1]
+      tf32_split(r1[SA1 + 8 * j + g], b2h[j][1], b2l[j][1]);
+    }
+    tf32_split(g < 4 ? r0[SXY + (g & 3)] : 0.0f, b0h[0], b0l[0]);  // B = [x y 1 0 ...]
+    tf32_split(g < 4 ? r1[SXY + (g & 3)] : 0.0f, b0h[1], b0l[1]);
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      mma_tf32(c1[0][j], a1h, b1h[j][0], b1h[j][1]);
+      mma_tf32(c2[0][j], a2h, b2h[j][0], b2h[j][1]);
+    }
+    mma_tf32(c0[0], a0h, b0h[0], b0h[1]);
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      mma_tf32(c1[1][j], a1h, b1l[j][0], b1l[j][1]);
+      mma_tf32(c2[1][j], a2h, b2l[j][0], b2l[j][1]);
+    }
+    mma_tf32(c0[1], a0h, b0l[0], b0l[1]);
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      mma_tf32(c1[2][j], a1l, b1h[j][0], b1h[j][1]);
+      mma_tf32(c2[2][j], a2l, b2h[j][0], b2h[j][1]);
+    }
+    mma_tf32(c0[2], a0l, b0h[0], b0h[1]);
+  }
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      c1[0][j][e] = __fadd_rn(c1[0][j][e], __fadd_rn(c1[1][j][e], c1[2][j][e]));
+      c2[0][j][e] = __fadd_rn(c2[0][j][e], __fadd_rn(c2[1][j][e], c2[2][j][e]));
+    }
+    c0[0][e] = __fadd_rn(c0[0][e], __fadd_rn(c0[1][e], c0[2][e]));
+  }
+  // C fragment: c[0] (row g, col 2tq), c[1] (g, 2tq+1), c[2] (g+8, 2tq), c[3] (g+8, 2tq+1)
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const int row = g + 8 * (e >> 1), colb = 2 * tq + (e & 1);
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int col = 8 * j + colb;
+      if (row < H) {  // gW1[o][k] and gb1[o] (ones column k == H)
+        if (col < H) pw[2 * H + row * H + col] += c1[0][j][e];
+        else if (col == H) pw[L::P + H + row] += c1[0][j][e];
+      }
+      if (row < 3) {  // gW2[j][k] and gb2[j]
+        if (col < H) pw[2 * H + H * H + row * H + col] += c2[0][j][e];
+        else if (col == H) pw[L::P + 2 * H + row] += c2[0][j][e];
+      }
+    }
+    if (row < H) {  // gW0[o][0..1] and gb0[o]
+      if (colb < 2) pw[2 * row + colb] += c0[0][e];
+      else if (colb == 2) pw[L::P + row] += c0[0][e];
+    }
+  }
+}
+
 template <int H, bool ACC, int NPX>
 __global__ void __launch_bounds__(kFitThreads / NPX, 1) fit_kernel(FitArgs A) {
   using L = FitLayout<H>;
@@ -313,68 +417,77 @@ __global__ void __launch_bounds__(kFitThreads / NPX, 1) fit_kernel(FitArgs A) {
           *reinterpret_cast<float4*>(row + SD0 + k) = make_float4(c0[p][k], c0[p][k + 1], c0[p][k + 2], c0[p][k + 3]);
         }
         *reinterpret_cast<float4*>(row + SD2) = make_float4(d2[p][0], d2[p][1], d2[p][2], 0.0f);
-        *reinterpret_cast<float4*>(row + SXY) = make_float4(x[p], y[p], 0.0f, 0.0f);
+        *reinterpret_cast<float4*>(row + SXY) = make_float4(x[p], y[p], 1.0f, 0.0f);
+        if constexpr (H < 16) {  // ones column: the tensor-core reduction also yields the bias gradients
+          row[SA0 + H] = 1.0f;
+          row[SA1 + H] = 1.0f;
+        }
       }
       __syncwarp();
       const int nq = HW - ch * CPX < CPX ? HW - ch * CPX : CPX;
+      if constexpr (H < 16) {
+        tc_reduce<H>(st, CPX, pw, lane);
+      } else {
       // per-lane accumulators live only for this chunk (uniform stream, see header)
-      float g8[8], g3[3], gq[3], gp = 0.0f, gu = 0.0f;
-#pragma unroll
-      for (int k = 0; k < 8; ++k) g8[k] = 0.0f;
-#pragma unroll
-      for (int j = 0; j < 3; ++j) g3[j] = gq[j] = 0.0f;
-      // lanes < 16: u = d1[o], vec = a0[0..7], p = d0[o], q = (x, y, 0)
-      // lanes >= 16: u = d1[o], vec = a0[8..15], p = a1[o], q = d2[0..2]
-      const int vo = hi_half ? SA0 + 8 : SA0;
-      const int po = hi_half ? SA1 + o16 : SD0 + o16;
-      const int qo = hi_half ? SD2 : SXY;
-      for (int q = 0; q < nq; ++q) {
-        const float* r = st + q * kStage;
-        const float u = r[SD1 + o16];
-        const float4 v0 = *reinterpret_cast<const float4*>(r + vo);
-        const float4 v1 = *reinterpret_cast<const float4*>(r + vo + 4);
-        const float p = r[po];
-        const float4 qq = *reinterpret_cast<const float4*>(r + qo);
-        g8[0] = fmaf(u, v0.x, g8[0]);
-        g8[1] = fmaf(u, v0.y, g8[1]);
-        g8[2] = fmaf(u, v0.z, g8[2]);
-        g8[3] = fmaf(u, v0.w, g8[3]);
-        g8[4] = fmaf(u, v1.x, g8[4]);
-        g8[5] = fmaf(u, v1.y, g8[5]);
-        g8[6] = fmaf(u, v1.z, g8[6]);
-        g8[7] = fmaf(u, v1.w, g8[7]);
-        g3[0] = fmaf(p, qq.x, g3[0]);
-        g3[1] = fmaf(p, qq.y, g3[1]);
-        g3[2] = fmaf(p, qq.z, g3[2]);
-        gp += p;
-        gu += u;
-        gq[0] += qq.x;
-        gq[1] += qq.y;
-        gq[2] += qq.z;
-      }
-      // fold into the warp's partial row; every canonical entry has one owner lane
-      {
-        const int o = o16;
-        if (o < H) {
-          if (!hi_half) {
-#pragma unroll
-            for (int k = 0; k < 8; ++k)
-              if (k < H) pw[2 * H + o * H + k] += g8[k];
-            pw[2 * o] += g3[0];
-            pw[2 * o + 1] += g3[1];
-            pw[L::P + o] += gp;      // b0
-            pw[L::P + H + o] += gu;  // b1
-          } else {
-#pragma unroll
-            for (int k = 0; k < 8; ++k)
-              if (8 + k < H) pw[2 * H + o * H + 8 + k] += g8[k];
-#pragma unroll
-            for (int j = 0; j < 3; ++j) pw[2 * H + H * H + j * H + o] += g3[j];
-            if (o == 0)
-#pragma unroll
-              for (int j = 0; j < 3; ++j) pw[L::P + 2 * H + j] += gq[j];
+        float g8[8], g3[3], gq[3], gp = 0.0f, gu = 0.0f;
+  #pragma unroll
+        for (int k = 0; k < 8; ++k) g8[k] = 0.0f;
+  #pragma unroll
+        for (int j = 0; j < 3; ++j) g3[j] = gq[j] = 0.0f;
+        // lanes < 16: u = d1[o], vec = a0[0..7], p = d0[o], q = (x, y, 0)
+        // lanes >= 16: u = d1[o], vec = a0[8..15], p = a1[o], q = d2[0..2]
+        const int vo = hi_half ? SA0 + 8 : SA0;
+        const int po = hi_half ? SA1 + o16 : SD0 + o16;
+        const int qo = hi_half ? SD2 : SXY;
+        for (int q = 0; q < nq; ++q) {
+          const float* r = st + q * kStage;
+          const float u = r[SD1 + o16];
+          const float4 v0 = *reinterpret_cast<const float4*>(r + vo);
+          const float4 v1 = *reinterpret_cast<const float4*>(r + vo + 4);
+          const float p = r[po];
+          const float4 qq = *reinterpret_cast<const float4*>(r + qo);
+          g8[0] = fmaf(u, v0.x, g8[0]);
+          g8[1] = fmaf(u, v0.y, g8[1]);
+          g8[2] = fmaf(u, v0.z, g8[2]);
+          g8[3] = fmaf(u, v0.w, g8[3]);
+          g8[4] = fmaf(u, v1.x, g8[4]);
+          g8[5] = fmaf(u, v1.y, g8[5]);
+          g8[6] = fmaf(u, v1.z, g8[6]);
+          g8[7] = fmaf(u, v1.w, g8[7]);
+          g3[0] = fmaf(p, qq.x, g3[0]);
+          g3[1] = fmaf(p, qq.y, g3[1]);
+          g3[2] = fmaf(p, qq.z, g3[2]);
+          gp += p;
+          gu += u;
+          gq[0] += qq.x;
+          gq[1] += qq.y;
+          gq[2] += qq.z;
+        }
+        // fold into the warp's partial row; every canonical entry has one owner lane
+        {
+          const int o = o16;
+          if (o < H) {
+            if (!hi_half) {
+  #pragma unroll
+              for (int k = 0; k < 8; ++k)
+                if (k < H) pw[2 * H + o * H + k] += g8[k];
+              pw[2 * o] += g3[0];
+              pw[2 * o + 1] += g3[1];
+              pw[L::P + o] += gp;      // b0
+              pw[L::P + H + o] += gu;  // b1
+            } else {
+  #pragma unroll
+              for (int k = 0; k < 8; ++k)
+                if (8 + k < H) pw[2 * H + o * H + 8 + k] += g8[k];
+  #pragma unroll
+              for (int j = 0; j < 3; ++j) pw[2 * H + H * H + j * H + o] += g3[j];
+              if (o == 0)
+  #pragma unroll
+                for (int j = 0; j < 3; ++j) pw[L::P + 2 * H + j] += gq[j];
+            }
           }
         }
+  
       }
       __syncwarp();
     }
