@@ -23,7 +23,10 @@ def __getattr__(name):
                 "CIFAR_MEAN", "CIFAR_STD"):
         from . import store
         return getattr(store, name)
-    if name in ("encoder", "transforms"):
+    if name in ("bench", "BenchReport"):
+        from . import harness
+        return getattr(harness, name)
+    if name in ("encoder", "transforms", "harness"):
         import importlib
         return importlib.import_module(f".{name}", __name__)
     if name in ("decode", "decode_batch", "install"):

@@ -78,7 +78,8 @@ def decode_batch(models, out_h: int | None = None, out_w: int | None = None, par
 
 def install(rinr_module=None) -> None:
     """Rebind ``rinr.decode``/``rinr.decode_batch`` (and the decoder
-    module's) to the GPU versions; results use rinr's own ImageBuffer."""
+    module's) and ``rinr.bench.bench`` to the GPU versions; results use
+    rinr's own ImageBuffer."""
     global _image_cls
     if rinr_module is None:
         import rinr as rinr_module  # noqa: PLC0415
@@ -89,3 +90,8 @@ def install(rinr_module=None) -> None:
     for mod in (rinr_module, dec_mod):
         mod.decode = decode
         mod.decode_batch = decode_batch
+    try:  # rinr.bench.bench -> the GPU harness (same BenchReport fields)
+        from .harness import bench as gpu_bench  # noqa: PLC0415
+        importlib.import_module(rinr_module.__name__ + ".bench").bench = gpu_bench
+    except ImportError:
+        pass

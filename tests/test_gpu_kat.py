@@ -104,3 +104,28 @@ def test_large_output_sampled(arch_name, precision):
                 assert float(np.abs(got - want).max()) <= 2e-2
             else:
                 assert float(np.abs(got - want).max()) <= 1e-3
+
+
+def test_bench_harness(golden, tmp_path):
+    """rinr.bench.bench mirror: report fields, stage keys, deterministic digest
+    that matches a digest of the same u8 pixels computed independently."""
+    import hashlib
+    from paper_2306_16699_b200 import Store, bench
+    data = golden("zoo")["archive"].tobytes()  # mixed architectures and native sizes
+    p = tmp_path / "zoo.rinr"
+    p.write_bytes(data)
+    r1 = bench(str(p), batch=3)
+    r2 = bench(data, batch=5, jobs=4)
+    models = O.read_models(data)
+    assert r1.images == len(models) and r1.pixels == sum(m.source_h * m.source_w for m in models)
+    assert set(r1.stage_seconds) == {"load", "dequantize", "forward", "clamp_convert"}
+    assert r1.digest == r2.digest and r1.images_per_s > 0
+    h = hashlib.sha256()
+    with Store(data) as st:
+        for k, m in enumerate(models):
+            u8 = st.decode(torch.tensor([k]), m.source_h, m.source_w, dtype=torch.uint8, layout="nhwc",
+                           precision="exact", sin="accurate").cpu().numpy()[0]
+            want = O.to_u8(O.decode(m))
+            assert np.abs(u8.astype(int) - want.astype(int)).max() <= 1
+            h.update(u8.tobytes())
+    assert h.hexdigest() == r1.digest
