@@ -37,6 +37,11 @@ typedef struct {
   double lr0;          /* cosine-decay peak (encoder.py:28-30)                  */
   double omega;        /* arch omega (net.py:21)                                 */
   int32_t curve_cap;   /* doubles per image in d_curve (>= steps/stride + 2)    */
+  const float* sched;  /* nullable device [steps][3] f32: per step t the values
+                          encoder._train and net.Adam use, f32(cosine_lr(lr0, t,
+                          steps)), f32(1 - 0.9**(t+1)), f32(1 - 0.999**(t+1)),
+                          computed on the host exactly as Python does; NULL:
+                          computed in the kernel (f64 pow / cos)                */
 } rinr_fit_params_t;
 
 /* Run `steps` Adam steps per image, updating d_w / d_b in place (masked

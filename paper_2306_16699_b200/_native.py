@@ -39,7 +39,7 @@ class StoreInfo(C.Structure):
 
 class FitParams(C.Structure):  # rinr_fit_params_t (include/rinr_b200_encoder.h)
     _fields_ = [("h", C.c_int32), ("w", C.c_int32), ("steps", C.c_int32), ("sin_mode", C.c_int32),
-                ("lr0", C.c_double), ("omega", C.c_double), ("curve_cap", C.c_int32)]
+                ("lr0", C.c_double), ("omega", C.c_double), ("curve_cap", C.c_int32), ("sched", C.c_void_p)]
 
 
 class DecodeParams(C.Structure):

@@ -78,6 +78,7 @@ struct FitArgs {
   float* grad_w;
   float* grad_b;
   double* loss0;
+  const float* sched;  // [steps][3] (lr, c1, c2) or null
 };
 
 template <bool ACC>
@@ -516,9 +517,16 @@ __global__ void __launch_bounds__(kFitThreads / NPX, 1) fit_kernel(FitArgs A) {
     }
     if (t == A.steps) break;
     // Adam step (net.py:282-296), numpy's f32 operation order
-    const double c1d = 1.0 - pow(0.9, double(t + 1)), c2d = 1.0 - pow(0.999, double(t + 1));
-    const float c1 = float(c1d), c2 = float(c2d);
-    const float lr = float(0.5 * A.lr0 * (1.0 + cos(3.141592653589793 * double(t) / double(A.steps))));
+    float lr, c1, c2;
+    if (A.sched) {
+      lr = A.sched[3 * t];
+      c1 = A.sched[3 * t + 1];
+      c2 = A.sched[3 * t + 2];
+    } else {
+      c1 = float(1.0 - pow(0.9, double(t + 1)));
+      c2 = float(1.0 - pow(0.999, double(t + 1)));
+      lr = float(0.5 * A.lr0 * (1.0 + cos(3.141592653589793 * double(t) / double(A.steps))));
+    }
     for (int p = tid; p < L::NPAR; p += NTH) {
       float g = 0.0f;
       for (int i = 0; i < NWP; ++i) g += part[i * L::NPAR_PAD + p];
@@ -656,6 +664,7 @@ extern "C" int rinr_fit(const int32_t* dims, int nl, int64_t n, float* d_w, floa
   a.grad_w = d_grad_w;
   a.grad_b = d_grad_b;
   a.loss0 = d_loss0;
+  a.sched = p->sched;
   const bool acc = p->sin_mode == RINR_SIN_ACCURATE;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   switch (H) {

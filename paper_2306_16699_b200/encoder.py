@@ -133,6 +133,17 @@ def init_batch(arch: Architecture, seeds, h: int, w: int, device="cuda") -> T.De
     return T.DeviceModels.from_batch(mb, device)
 
 
+def _schedule(lr0: float, steps: int) -> np.ndarray:
+    """[steps, 3] f32: the learning rate and Adam bias corrections of every
+    step, computed exactly as encoder._train / net.Adam do (Python floats,
+    cast to f32 where numpy's weak scalars meet the f32 arrays)."""
+    t = np.arange(steps)
+    lr = np.array([cosine_lr(lr0, int(i), steps) for i in t], np.float64)
+    c1 = np.array([1.0 - 0.9 ** int(i + 1) for i in t], np.float64)
+    c2 = np.array([1.0 - 0.999 ** int(i + 1) for i in t], np.float64)
+    return np.stack([lr, c1, c2], 1).astype(np.float32)
+
+
 def train_batch(dm: T.DeviceModels, images: torch.Tensor, lr0: float, steps: int, sin: str = "mufu"):
     """encoder._train for every model/image pair (in place).  Returns
     (curves [N, k] f64 numpy, status [N] int: 0 or failing step + 1)."""
@@ -141,7 +152,8 @@ def train_batch(dm: T.DeviceModels, images: torch.Tensor, lr0: float, steps: int
     cap = (steps + stride - 1) // stride + 2
     curve = torch.empty((n, cap), dtype=torch.float64, device=images.device)
     status = torch.zeros(n, dtype=torch.int32, device=images.device)
-    p = FitParams(h, w, steps, SIN_MODES[sin], float(lr0), float(dm.arch.omega), cap)
+    sched = torch.from_numpy(_schedule(lr0, steps)).to(images.device)
+    p = FitParams(h, w, steps, SIN_MODES[sin], float(lr0), float(dm.arch.omega), cap, sched.data_ptr())
     dims, nl = T._dims(dm.arch)
     N.check(_lib().rinr_fit(dims, nl, n, dm.w.data_ptr(), dm.b.data_ptr(), dm.mask.data_ptr(), images.data_ptr(),
                             C.byref(p), curve.data_ptr(), status.data_ptr(), None, None, None,
@@ -158,7 +170,7 @@ def loss_and_grad_batch(dm: T.DeviceModels, images: torch.Tensor, sin: str = "mu
     loss = torch.empty(n, dtype=torch.float64, device=images.device)
     curve = torch.empty((n, 2), dtype=torch.float64, device=images.device)
     status = torch.zeros(n, dtype=torch.int32, device=images.device)
-    p = FitParams(h, w, 0, SIN_MODES[sin], 0.0, float(dm.arch.omega), 2)
+    p = FitParams(h, w, 0, SIN_MODES[sin], 0.0, float(dm.arch.omega), 2, None)
     dims, nl = T._dims(dm.arch)
     N.check(_lib().rinr_fit(dims, nl, n, dm.w.data_ptr(), dm.b.data_ptr(), dm.mask.data_ptr(), images.data_ptr(),
                             C.byref(p), curve.data_ptr(), status.data_ptr(), gw.data_ptr(), gb.data_ptr(),
