@@ -201,6 +201,16 @@ def quantize(model, mode: str) -> InrModel:
     return quantize_batch(ModelBatch.from_models([model]), mode).model(0)
 
 
+def to_half(model):
+    """Cast all weight matrices to float16, biases stay float32 (compressor.py:236-246)."""
+    if getattr(model, "quant", None) is not None:
+        raise FormatError("cast before quantizing, not after")
+    out = model.copy()
+    for lw in out.layers:
+        lw.w = lw.w.astype(np.float16)
+    return out
+
+
 def dequantize(model):
     """Validate quantisation metadata and drop it (compressor.py:221-235)."""
     if model.quant is None:
