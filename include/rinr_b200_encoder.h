@@ -5,7 +5,7 @@
  *
  * Models use the transform layout of rinr_b200_transforms.h: d_w [n][P] f32
  * (matrices concatenated, row-major (out, in)), d_b [n][sum dims[1..]] f32,
- * d_mask [n][P] u8.  Supported architectures: (2, H, H, 3) with 8 <= H <= 16
+ * d_mask [n][P] u8.  Supported architectures: (2, H, H, 3) with 8 <= H <= 16 (all widths built)
  * (the CIFAR net of PAPER.md:441 is H = 15); others return
  * RINR_ERR_UNSUPPORTED.
  *

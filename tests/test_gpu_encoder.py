@@ -122,3 +122,27 @@ def test_unsupported(E):
     dm = E.init_batch(E.Architecture((2, 20, 20, 3)), [0], 8, 8)
     with pytest.raises(UnsupportedError):
         E.train_batch(dm, torch.zeros((1, 8, 8, 3), device="cuda"), 1e-3, 2)
+
+
+@pytest.mark.parametrize("H", [8, 9, 12, 13, 14, 16])
+def test_widths_vs_oracle(E, H):
+    """Every supported hidden width: the first step's loss and gradients
+    match the oracle's net.loss_and_grad restatement; a short fit stays finite."""
+    from oracle import rinr_oracle as O
+    from transforms_common import cat, smooth_images
+    dims = (2, H, H, 3)
+    x = smooth_images(2, 12, 20, seed=H)
+    dm = E.init_batch(E.Architecture(dims), [H, H + 1], 12, 20)
+    img = torch.from_numpy(x).cuda()
+    loss, gw, gb = E.loss_and_grad_batch(dm, img, "accurate")
+    coords = O.coordinate_grid(12, 20)
+    for i in range(2):
+        ws, bs, ms = O.init_model(dims, [H, H + 1][i])
+        ref_loss, gws, gbs = O.loss_and_grad(ws, bs, ms, 30.0, coords, x[i].reshape(-1, 3))
+        assert abs(loss[i].item() - ref_loss) <= 1e-5 * ref_loss
+        a, b = gw[i].cpu().numpy(), cat(gws)
+        assert np.linalg.norm(a - b) <= 1e-4 * np.linalg.norm(b)
+        a, b = gb[i].cpu().numpy(), cat(gbs)
+        assert np.linalg.norm(a - b) <= 1e-4 * np.linalg.norm(b) + 1e-12
+    curves, status = E.train_batch(dm, img, 5e-4, 30)
+    assert not status.any() and np.isfinite(curves[~np.isnan(curves)]).all()
