@@ -6,8 +6,10 @@
 
 #include <cstdio>
 #include <cstring>
+#include <algorithm>
 #include <memory>
 #include <string>
+#include <thread>
 #include <unordered_set>
 #include <vector>
 
@@ -187,29 +189,58 @@ static void parse_archive(const uint8_t* data, size_t len, uint32_t rank, uint32
                                                " != expected " + std::to_string(expect)};
     expect = off + length;
   }
-  // ... then each record's bytes, CRC and parse in order (read_raw, archive.py:369-379) ...
+  // ... then each record's bytes, CRC and parse (read_raw, archive.py:369-379).
+  // Records are independent, so contiguous ranges run on host threads; each
+  // thread stops at its first failure and the lowest-index failure is raised,
+  // which is exactly the record the reference's in-order loop reports.
+  std::vector<ParsedRecord> all(count);
+  auto check_range = [&](uint32_t k0, uint32_t k1, int64_t& bad, ParseError& err) {
+    for (uint32_t k = k0; k < k1; ++k) {
+      try {
+        uint64_t off = rd<uint64_t>(data + 10 + 12 * size_t(k));
+        uint32_t length = rd<uint32_t>(data + 10 + 12 * size_t(k) + 8);
+        std::string ctx = "record " + std::to_string(k);
+        if (off + length > len) throw ParseError{RINR_ERR_INTEGRITY, ctx + ": truncated body"};
+        if (length < 4) throw ParseError{RINR_ERR_INTEGRITY, ctx + ": record too short for CRC"};
+        const uint8_t* blob = data + off;
+        uint32_t stored = rd<uint32_t>(blob + length - 4);
+        uint32_t actual = crc32(blob, length - 4);
+        if (stored != actual) {
+          char buf[96];
+          std::snprintf(buf, sizeof buf, ": CRC mismatch (stored %#010x, computed %#010x)", stored, actual);
+          throw ParseError{RINR_ERR_INTEGRITY, ctx + buf};
+        }
+        parse_body(blob, length - 4, ctx, all[k]);
+        all[k].body_off = off;
+      } catch (const ParseError& e) {
+        bad = k;
+        err = e;
+        return;
+      }
+    }
+  };
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const uint32_t nthr = count < 4096 ? 1u : std::min<uint32_t>(std::min(hw, 32u), count / 2048);
+  std::vector<int64_t> bad(nthr, -1);
+  std::vector<ParseError> errs(nthr);
+  if (nthr == 1) {
+    check_range(0, count, bad[0], errs[0]);
+  } else {
+    std::vector<std::thread> pool;
+    for (uint32_t t = 0; t < nthr; ++t) {
+      const uint32_t k0 = uint32_t(uint64_t(count) * t / nthr), k1 = uint32_t(uint64_t(count) * (t + 1) / nthr);
+      pool.emplace_back(check_range, k0, k1, std::ref(bad[t]), std::ref(errs[t]));
+    }
+    for (auto& th : pool) th.join();
+  }
+  for (uint32_t t = 0; t < nthr; ++t)  // ranges are in index order: the first failing range holds the first failure
+    if (bad[t] >= 0) throw errs[t];
   std::vector<std::string> all_ids;
   all_ids.reserve(count);
   for (uint32_t k = 0; k < count; ++k) {
-    uint64_t off = rd<uint64_t>(data + 10 + 12 * size_t(k));
-    uint32_t length = rd<uint32_t>(data + 10 + 12 * size_t(k) + 8);
-    std::string ctx = "record " + std::to_string(k);
-    if (off + length > len) throw ParseError{RINR_ERR_INTEGRITY, ctx + ": truncated body"};
-    if (length < 4) throw ParseError{RINR_ERR_INTEGRITY, ctx + ": record too short for CRC"};
-    const uint8_t* blob = data + off;
-    uint32_t stored = rd<uint32_t>(blob + length - 4);
-    uint32_t actual = crc32(blob, length - 4);
-    if (stored != actual) {
-      char buf[96];
-      std::snprintf(buf, sizeof buf, ": CRC mismatch (stored %#010x, computed %#010x)", stored, actual);
-      throw ParseError{RINR_ERR_INTEGRITY, ctx + buf};
-    }
-    ParsedRecord pr;
-    parse_body(blob, length - 4, ctx, pr);
-    pr.body_off = off;
-    all_ids.push_back(pr.id);
+    all_ids.push_back(all[k].id);
     if (keep && k % world == rank) {
-      pa.recs.push_back(std::move(pr));
+      pa.recs.push_back(std::move(all[k]));
       pa.global.push_back(k);
     }
   }

@@ -101,3 +101,18 @@ def test_error_is_thread_local():
 def _tiny():
     from paper_2306_16699_b200 import synth
     return synth.archive_bytes(synth.seeded_batch(synth.ARCH_A, [0]))
+
+
+def test_threaded_validation_reports_first_failure():
+    """Archives of >= 4096 records are checked on host threads; the error is
+    still the first failing record in index order (archive.py:369-379)."""
+    from paper_2306_16699_b200 import IntegrityError, synth
+    mb = synth.tweak_r1(synth.random_batch(synth.ARCH_A, 10000, seed=4))
+    data = bytearray(synth.archive_bytes(mb))
+    assert N.archive_validate(bytes(data)) == 10000
+    for k in (7000, 3000):  # flip one byte inside each record's body
+        off, length = struct.unpack_from("<QI", data, 10 + 12 * k)
+        data[off + length // 2] ^= 0xFF
+    with pytest.raises(IntegrityError) as e:
+        N.archive_validate(bytes(data))
+    assert "record 3000" in str(e.value)
