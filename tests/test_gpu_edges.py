@@ -1,0 +1,66 @@
+"""Edge cases of the Store.decode / rinr_decode boundary: empty and
+single-pixel outputs, very large batches, repeated ids, ids given as CPU
+tensors / lists / int32, and out-of-range ids anywhere in a large batch."""
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import rinr_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def c2():
+    from paper_2306_16699_b200 import Store, synth
+    data = synth.archive_bytes(synth.config2(64, seed=5))
+    st = Store(data)
+    yield st, O.read_models(data)
+    st.close()
+
+
+def test_empty_batch(c2):
+    st, _ = c2
+    out = st.decode(torch.zeros(0, dtype=torch.int64), 32, 32)
+    assert out.shape == (0, 3, 32, 32)
+
+
+def test_one_pixel_and_thin_outputs(c2):
+    st, models = c2
+    for h, w in ((1, 1), (1, 64), (64, 1), (3, 2)):
+        got = st.decode(torch.arange(8), h, w, layout="nhwc").cpu().numpy()
+        for i in range(8):
+            assert float(np.abs(got[i] - O.decode(models[i], h, w)).max()) <= 1e-3
+
+
+def test_ids_forms_and_repeats(c2):
+    st, models = c2
+    want = st.decode(torch.tensor([3, 3, 7, 0]), 32, 32).cpu()
+    for ids in ([3, 3, 7, 0], np.array([3, 3, 7, 0], np.int32), torch.tensor([3, 3, 7, 0], dtype=torch.int32),
+                torch.tensor([0, 3, 9, 3, 11, 7, 5, 0])[[1, 3, 5, 0]]):
+        assert torch.equal(st.decode(ids, 32, 32).cpu(), want)
+    assert torch.equal(want[0], want[1])
+
+
+def test_large_batch_matches_small(c2):
+    """65,536 ids (many images per CTA, several phase-1 chunks): every image
+    equals its decode in a 1-image batch (bitwise, same kernels)."""
+    st, _ = c2
+    g = torch.Generator().manual_seed(0)
+    ids = torch.randint(0, 64, (65536,), generator=g)
+    out = st.decode(ids, 32, 32)
+    single = st.decode(torch.arange(64), 32, 32)
+    for pos in (0, 1, 12345, 40000, 65535):
+        assert torch.equal(out[pos], single[int(ids[pos])])
+
+
+def test_bad_id_in_large_batch(c2):
+    from paper_2306_16699_b200 import BatchItemError
+    st, _ = c2
+    ids = torch.randint(0, 64, (20000,))
+    ids[15000] = 64
+    ids[17000] = -5
+    with pytest.raises(BatchItemError) as e:
+        st.decode(ids, 32, 32)
+    assert e.value.index == 15000
