@@ -29,6 +29,9 @@
 namespace rinr {
 namespace {
 
+#ifndef RINR_FIT_NPX
+#define RINR_FIT_NPX 2  // pixels per thread
+#endif
 constexpr int kFitWarps = 16;
 constexpr int kFitThreads = kFitWarps * 32;
 constexpr int kStage = 76;  // floats per staged pixel (stride 76: conflict-free STS.128)
@@ -43,8 +46,11 @@ struct FitLayout {
   static constexpr int NPAR = P + PB;
   static constexpr int NPAR_PAD = (NPAR + 3) & ~3;
   // shared compute copy (padded rows)
+  // W1TS: a transposed copy of W1 (column k at W1TS + 16k), so layer 1 runs
+  // k-outer with H independent accumulators per pixel instead of H-long chains
   static constexpr int W0S = 0, W1S = 32, W2S = 32 + 256, B0S = W2S + 64, B1S = B0S + 16, B2S = B1S + 16;
-  static constexpr int WS = B2S + 16;
+  static constexpr int W1TS = B2S + 16;
+  static constexpr int WS = W1TS + 256;
   __device__ static int slot(int p) {
     if (p < 2 * H) return W0S + p;  // row o = p/2 of 2 floats
     p -= 2 * H;
@@ -56,6 +62,12 @@ struct FitLayout {
     p -= H;
     if (p < H) return B1S + p;
     return B2S + (p - H);
+  }
+  // store parameter p (canonical order) into the compute copy, W1 twice
+  __device__ static void put(float* ws, int p, float v) {
+    ws[slot(p)] = v;
+    const int q = p - 2 * H;
+    if (q >= 0 && q < H * H) ws[W1TS + (q % H) * 16 + q / H] = v;
   }
   static constexpr size_t smem_bytes(int npx) {
     return sizeof(float) * (size_t(WS) + 2 * NPAR_PAD + ((P + 3) & ~3) + size_t(kFitWarps / npx) * NPAR_PAD +
@@ -144,18 +156,27 @@ __device__ __forceinline__ void pixel_pass(const float* __restrict__ ws, const f
       }
     }
   }
-  // layer 1: H -> H
+  // layer 1: H -> H, k-outer over W1's columns: NPX*H independent FMA
+  // chains, each summing k = 0..H-1 in order (the same rounding as a dot loop)
+#pragma unroll
+  for (int p = 0; p < NPX; ++p)
+#pragma unroll
+    for (int o = 0; o < 16; ++o) a1[p][o] = 0.0f;
+#pragma unroll
+  for (int k = 0; k < H; ++k) {
+    wrow<H>(ws + L::W1TS + 16 * k, r);
+#pragma unroll
+    for (int p = 0; p < NPX; ++p)
+#pragma unroll
+      for (int o = 0; o < H; ++o) a1[p][o] = fmaf(a0[p][k], r[o], a1[p][o]);
+  }
   wrow<H>(ws + L::B1S, bb);
 #pragma unroll
   for (int o = 0; o < H; ++o) {
-    wrow<H>(ws + L::W1S + 16 * o, r);
 #pragma unroll
     for (int p = 0; p < NPX; ++p) {
-      float acc = 0.0f;
-#pragma unroll
-      for (int k = 0; k < H; ++k) acc = fmaf(a0[p][k], r[k], acc);
       float s, c;
-      sincos_<ACC>(__fmul_rn(om, __fadd_rn(acc, bb[o])), s, c);
+      sincos_<ACC>(__fmul_rn(om, __fadd_rn(a1[p][o], bb[o])), s, c);
       a1[p][o] = s;
       c1[p][o] = __fmul_rn(om, c);
     }
@@ -238,7 +259,9 @@ __device__ __forceinline__ void tf32_split(float x, uint32_t& hi, uint32_t& lo) 
 }
 
 // Outer-product gradient sums of one staged chunk on tensor cores (H < 16):
-//   gW1 | gb1 = d1^T [a0 | 1],   gW2 | gb2 = d2^T [a1 | 1],   gW0 | gb0 = d0^T [x y 1]
+//   gW1 | gb1 = d1^T [a0 | 1],   (gW2 | gb2)^T = [a1 | 1]^T d2,   gW0 | gb0 = d0^T [x y 1]
+// (gW2 is computed transposed so its 3 rows fill one N = 8 tile instead of
+// padding M = 16 over two tiles: 12 MMAs per 8 pixels instead of 15)
 // as M16 x N x K(=pixels) GEMMs in 3xTF32 (hi*hi + hi*lo + lo*hi), then the
 // fragments are added to the warp's partial row (each entry has one owner lane).
 template <int H>
@@ -246,12 +269,12 @@ __device__ __forceinline__ void tc_reduce(const float* st, int rows, float* pw, 
   using L = FitLayout<H>;
   const int g = lane >> 2, tq = lane & 3;
   // one accumulator per 3xTF32 pass: 15 independent MMA chains per k-step
-  float c1[3][2][4] = {}, c2[3][2][4] = {}, c0[3][4] = {};
+  float c1[3][2][4] = {}, c2[3][4] = {}, c0[3][4] = {};
   for (int kb = 0; kb < rows; kb += 8) {
     const float* r0 = st + (kb + tq) * kStage;      // pixel kb + tq
     const float* r1 = st + (kb + tq + 4) * kStage;  // pixel kb + tq + 4
-    // A operands (rows = output unit, K = pixel): d1^T, d0^T, d2^T
-    uint32_t a1h[4], a1l[4], a0h[4], a0l[4], a2h[4], a2l[4];
+    // A operands (rows = unit, K = pixel): d1^T, d0^T; d2 is a B operand (N = j)
+    uint32_t a1h[4], a1l[4], a0h[4], a0l[4], d2h[2], d2l[2];
     tf32_split(r0[SD1 + g], a1h[0], a1l[0]);
     tf32_split(r0[SD1 + g + 8], a1h[1], a1l[1]);
     tf32_split(r1[SD1 + g], a1h[2], a1l[2]);
@@ -260,46 +283,39 @@ __device__ __forceinline__ void tc_reduce(const float* st, int rows, float* pw, 
     tf32_split(r0[SD0 + g + 8], a0h[1], a0l[1]);
     tf32_split(r1[SD0 + g], a0h[2], a0l[2]);
     tf32_split(r1[SD0 + g + 8], a0h[3], a0l[3]);
-    tf32_split(g < 3 ? r0[SD2 + (g & 3)] : 0.0f, a2h[0], a2l[0]);
-    a2h[1] = a2l[1] = 0u;
-    tf32_split(g < 3 ? r1[SD2 + (g & 3)] : 0.0f, a2h[2], a2l[2]);
-    a2h[3] = a2l[3] = 0u;
+    tf32_split(g < 3 ? r0[SD2 + (g & 3)] : 0.0f, d2h[0], d2l[0]);
+    tf32_split(g < 3 ? r1[SD2 + (g & 3)] : 0.0f, d2h[1], d2l[1]);
     uint32_t b1h[2][2], b1l[2][2], b2h[2][2], b2l[2][2], b0h[2], b0l[2];
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       tf32_split(r0[SA0 + 8 * j + g], b1h[j][0], b1l[j][0]);  // B = [a0 | 1]
       tf32_split(r1[SA0 + 8 * j + g], b1h[j][1], b1l[j][1]);
-      tf32_split(r0[SA1 + 8 * j + g], b2h[j][0], b2l[j][0]);  // B = [a1 | 1]
+      tf32_split(r0[SA1 + 8 * j + g], b2h[j][0], b2l[j][0]);  // [a1 | 1] (gW2^T A operand)
       tf32_split(r1[SA1 + 8 * j + g], b2h[j][1], b2l[j][1]);
     }
     tf32_split(g < 4 ? r0[SXY + (g & 3)] : 0.0f, b0h[0], b0l[0]);  // B = [x y 1 0 ...]
     tf32_split(g < 4 ? r1[SXY + (g & 3)] : 0.0f, b0h[1], b0l[1]);
+    // A = [a1 | 1]^T: the B values loaded for gW2 before, regrouped
+    const uint32_t e2h[4] = {b2h[0][0], b2h[1][0], b2h[0][1], b2h[1][1]};
+    const uint32_t e2l[4] = {b2l[0][0], b2l[1][0], b2l[0][1], b2l[1][1]};
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      mma_tf32(c1[0][j], a1h, b1h[j][0], b1h[j][1]);
-      mma_tf32(c2[0][j], a2h, b2h[j][0], b2h[j][1]);
-    }
+    for (int j = 0; j < 2; ++j) mma_tf32(c1[0][j], a1h, b1h[j][0], b1h[j][1]);
+    mma_tf32(c2[0], e2h, d2h[0], d2h[1]);
     mma_tf32(c0[0], a0h, b0h[0], b0h[1]);
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      mma_tf32(c1[1][j], a1h, b1l[j][0], b1l[j][1]);
-      mma_tf32(c2[1][j], a2h, b2l[j][0], b2l[j][1]);
-    }
+    for (int j = 0; j < 2; ++j) mma_tf32(c1[1][j], a1h, b1l[j][0], b1l[j][1]);
+    mma_tf32(c2[1], e2h, d2l[0], d2l[1]);
     mma_tf32(c0[1], a0h, b0l[0], b0l[1]);
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      mma_tf32(c1[2][j], a1l, b1h[j][0], b1h[j][1]);
-      mma_tf32(c2[2][j], a2l, b2h[j][0], b2h[j][1]);
-    }
+    for (int j = 0; j < 2; ++j) mma_tf32(c1[2][j], a1l, b1h[j][0], b1h[j][1]);
+    mma_tf32(c2[2], e2l, d2h[0], d2h[1]);
     mma_tf32(c0[2], a0l, b0h[0], b0h[1]);
   }
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
 #pragma unroll
-    for (int j = 0; j < 2; ++j) {
-      c1[0][j][e] = __fadd_rn(c1[0][j][e], __fadd_rn(c1[1][j][e], c1[2][j][e]));
-      c2[0][j][e] = __fadd_rn(c2[0][j][e], __fadd_rn(c2[1][j][e], c2[2][j][e]));
-    }
+    for (int j = 0; j < 2; ++j) c1[0][j][e] = __fadd_rn(c1[0][j][e], __fadd_rn(c1[1][j][e], c1[2][j][e]));
+    c2[0][e] = __fadd_rn(c2[0][e], __fadd_rn(c2[1][e], c2[2][e]));
     c0[0][e] = __fadd_rn(c0[0][e], __fadd_rn(c0[1][e], c0[2][e]));
   }
   // C fragment: c[0] (row g, col 2tq), c[1] (g, 2tq+1), c[2] (g+8, 2tq), c[3] (g+8, 2tq+1)
@@ -313,10 +329,10 @@ __device__ __forceinline__ void tc_reduce(const float* st, int rows, float* pw, 
         if (col < H) pw[2 * H + row * H + col] += c1[0][j][e];
         else if (col == H) pw[L::P + H + row] += c1[0][j][e];
       }
-      if (row < 3) {  // gW2[j][k] and gb2[j]
-        if (col < H) pw[2 * H + H * H + row * H + col] += c2[0][j][e];
-        else if (col == H) pw[L::P + 2 * H + row] += c2[0][j][e];
-      }
+    }
+    if (colb < 3) {  // transposed: row = unit k of a1 (k == H: gb2), col = output j
+      if (row < H) pw[2 * H + H * H + colb * H + row] += c2[0][e];
+      else if (row == H) pw[L::P + 2 * H + colb] += c2[0][e];
     }
     if (row < H) {  // gW0[o][0..1] and gb0[o]
       if (colb < 2) pw[2 * row + colb] += c0[0][e];
@@ -347,7 +363,7 @@ __global__ void __launch_bounds__(kFitThreads / NPX, 1) fit_kernel(FitArgs A) {
   for (int i = tid; i < L::WS; i += NTH) ws[i] = 0.0f;
   __syncthreads();
   for (int p = tid; p < L::NPAR; p += NTH) {
-    ws[L::slot(p)] = p < L::P ? gw[p] : gb[p - L::P];
+    L::put(ws, p, p < L::P ? gw[p] : gb[p - L::P]);
     mo[p] = 0.0f;
     ve[p] = 0.0f;
     if (p < L::P) mk[p] = A.mask[m * L::P + p] ? 1.0f : 0.0f;
@@ -539,7 +555,7 @@ __global__ void __launch_bounds__(kFitThreads / NPX, 1) fit_kernel(FitArgs A) {
       const float upd = __fdiv_rn(__fmul_rn(lr, __fdiv_rn(mp, c1)), __fadd_rn(__fsqrt_rn(__fdiv_rn(vp, c2)), 1e-8f));
       float w = __fsub_rn(ws[s], upd);
       if (p < L::P) w = __fmul_rn(w, mk[p]);  // np.multiply(layer.w, mask)
-      ws[s] = w;
+      L::put(ws, p, w);
     }
     __syncthreads();
   }
@@ -564,7 +580,7 @@ __global__ void __launch_bounds__(256) render_kernel(int64_t n, const float* __r
   const int64_t m = blockIdx.y;
   for (int i = threadIdx.x; i < L::WS; i += 256) ws[i] = 0.0f;
   __syncthreads();
-  for (int p = threadIdx.x; p < L::NPAR; p += 256) ws[L::slot(p)] = p < L::P ? w[m * L::P + p] : b[m * L::PB + p - L::P];
+  for (int p = threadIdx.x; p < L::NPAR; p += 256) L::put(ws, p, p < L::P ? w[m * L::P + p] : b[m * L::PB + p - L::P]);
   __syncthreads();
   const int HW = h * wd;
   const int px = blockIdx.x * 256 + threadIdx.x;
@@ -608,7 +624,7 @@ int launch_fit(const FitArgs& a, cudaStream_t st) {
 // serves two pixels (one pixel per thread with 16 warps measured 6% slower)
 template <int H>
 int dispatch_fit(const FitArgs& a, bool acc, cudaStream_t st) {
-  return acc ? launch_fit<H, true, 2>(a, st) : launch_fit<H, false, 2>(a, st);
+  return acc ? launch_fit<H, true, RINR_FIT_NPX>(a, st) : launch_fit<H, false, RINR_FIT_NPX>(a, st);
 }
 
 template <int H, bool ACC>
