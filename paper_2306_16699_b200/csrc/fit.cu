@@ -24,6 +24,7 @@
 
 #include "../../include/rinr_b200_encoder.h"
 #include "device_common.cuh"
+#include "mma_chain.cuh"
 #include "rinr_internal.h"
 
 namespace rinr {
@@ -69,9 +70,10 @@ struct FitLayout {
     const int q = p - 2 * H;
     if (q >= 0 && q < H * H) ws[W1TS + (q % H) * 16 + q / H] = v;
   }
-  static constexpr size_t smem_bytes(int npx) {
+  // fixed part; the MMA pass adds no staging tiles but (h + w) coordinate floats
+  static constexpr size_t smem_bytes(int npx, bool stage = true) {
     return sizeof(float) * (size_t(WS) + 2 * NPAR_PAD + ((P + 3) & ~3) + size_t(kFitWarps / npx) * NPAR_PAD +
-                            size_t(kFitWarps / npx) * 32 * npx * kStage) +
+                            (stage ? size_t(kFitWarps / npx) * 32 * npx * kStage : 0)) +
            sizeof(double) * kFitWarps;
   }
 };
@@ -341,8 +343,291 @@ __device__ __forceinline__ void tc_reduce(const float* st, int rows, float* pw, 
   }
 }
 
-template <int H, bool ACC, int NPX>
+// ---------------------------------------------------------------------------
+// Tensor-core pixel pass (MUFU sine mode, H < 16): pixel_pass's per-pixel
+// network as register-resident mma.sync.m16n8k16 chains, like the decoder's
+// (mma_chain.cuh).  A warp evaluates 16-pixel m-tiles; the f32 accumulator
+// fragment of n-tiles 0 / 1 is the A fragment of the next product, so
+//   z1 = a0 W1^T + b1,  out = a1 W2^T + b2,  d1 = (d2 W2) * c1,  d0 = (d1 W1) * c0
+// never leave registers.  Products are bf16 3-pass (Ah*Bh + Al*Bh + Ah*Bl,
+// truncation split: about 2^-16 relative per product), inside the MUFU mode's
+// stated gradient tolerance; the accurate-sine mode keeps the fp32 FFMA pass.
+// Layer 0 (K = 2) is FFMA in the same fragment layout.  C-fragment element e
+// of n-tile j: pixel row g + 8(e >> 1), unit 8j + 2tq + (e & 1).
+// ---------------------------------------------------------------------------
+struct FitFrags {
+  uint32_t w1f[2][4];  // forward B[k][n] = W1[n][k]: {b0 hi, b1 hi, b0 lo, b1 lo} per n-tile
+  uint32_t w1b[2][4];  // backward B[o][k] = W1[o][k]
+  uint32_t w2f[4];     // forward B[k][j] = W2[j][k] (3 valid columns)
+  uint32_t w2b[2][2];  // backward B[j][o] = W2[j][o] (K = 3 valid): {hi, lo}
+  float w0x[2][2], w0y[2][2], b0[2][2], b1[2][2], b2[2];  // this lane's units / outputs
+};
+
+template <int H>
+__device__ __forceinline__ void load_frags(const float* ws, int lane, FitFrags& F) {
+  using L = FitLayout<H>;
+  const int g = lane >> 2, tq = lane & 3;
+  // W1 rows are zero padded to 16 x 16, W2 to 4 x 16 (ws is zeroed at start)
+  auto W1 = [&](int o, int k) { return ws[L::W1S + 16 * o + k]; };
+  auto W2 = [&](int j, int k) { return j < 3 ? ws[L::W2S + 16 * j + k] : 0.0f; };
+#pragma unroll
+  for (int j = 0; j < 2; ++j) {
+    const int n = 8 * j + g;
+    pack_act<true>(W1(n, 2 * tq), W1(n, 2 * tq + 1), F.w1f[j][0], F.w1f[j][2]);
+    pack_act<true>(W1(n, 2 * tq + 8), W1(n, 2 * tq + 9), F.w1f[j][1], F.w1f[j][3]);
+    pack_act<true>(W1(2 * tq, n), W1(2 * tq + 1, n), F.w1b[j][0], F.w1b[j][2]);
+    pack_act<true>(W1(2 * tq + 8, n), W1(2 * tq + 9, n), F.w1b[j][1], F.w1b[j][3]);
+    pack_act<true>(W2(2 * tq, n), W2(2 * tq + 1, n), F.w2b[j][0], F.w2b[j][1]);
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int u = 8 * j + 2 * tq + e;
+      F.w0x[j][e] = ws[L::W0S + 2 * u];
+      F.w0y[j][e] = ws[L::W0S + 2 * u + 1];
+      F.b0[j][e] = ws[L::B0S + u];
+      F.b1[j][e] = ws[L::B1S + u];
+    }
+  }
+  pack_act<true>(W2(g, 2 * tq), W2(g, 2 * tq + 1), F.w2f[0], F.w2f[2]);
+  pack_act<true>(W2(g, 2 * tq + 8), W2(g, 2 * tq + 9), F.w2f[1], F.w2f[3]);
+  F.b2[0] = ws[L::B2S + 2 * tq];  // zero beyond the 3 outputs
+  F.b2[1] = ws[L::B2S + 2 * tq + 1];
+}
+
+// A fragment (hi, lo) of a 16 x 16 activation tile held as two n-tile accumulators
+__device__ __forceinline__ void frag_a(const float (&v)[2][4], uint32_t (&hi)[4], uint32_t (&lo)[4]) {
+  pack_act<true>(v[0][0], v[0][1], hi[0], lo[0]);
+  pack_act<true>(v[0][2], v[0][3], hi[1], lo[1]);
+  pack_act<true>(v[1][0], v[1][1], hi[2], lo[2]);
+  pack_act<true>(v[1][2], v[1][3], hi[3], lo[3]);
+}
+
+// c += A * B in three bf16 passes (B given as {b0 hi, b1 hi, b0 lo, b1 lo})
+__device__ __forceinline__ void mma3(float (&c)[4], const uint32_t (&ah)[4], const uint32_t (&al)[4],
+                                     const uint32_t (&b)[4]) {
+  mma16816(c, ah, b[0], b[1]);
+  mma16816(c, al, b[0], b[1]);
+  mma16816(c, ah, b[2], b[3]);
+}
+
+// Transpose of an 8 x 8 bf16 block held one row per 4 lanes (C / A fragment
+// quarter) into the B-fragment orientation: lane (g, tq) receives rows
+// 2tq, 2tq+1 of column g.
+__device__ __forceinline__ uint32_t movt(uint32_t x) {
+  uint32_t y;
+  asm("movmatrix.sync.aligned.m8n8.trans.b16 %0, %1;" : "=r"(y) : "r"(x));
+  return y;
+}
+
+// Per-warp gradient sums of one step, as MMA accumulators (K = pixels):
+//   w1[j]: gW1 | gb1 = d1^T [a0 | 1]  rows o = g + 8(e>>1), cols k = 8j + 2tq + (e&1)
+//   w2t:   (gW2 | gb2)^T = [a1 | 1]^T d2  rows k, cols output j
+//   w0:    gW0 | gb0 = d0^T [x y 1]   rows o, cols (x, y, 1)
+struct FitGrads {
+  float w1[2][4], w2t[4], w0[4];
+};
+
+// {A^T} of a 16 x 16 tile given as A-fragment words (rows = pixels): the
+// A fragment of its transpose (rows = units, K = pixels)
+__device__ __forceinline__ void frag_at(const uint32_t (&p)[4], uint32_t (&t)[4]) {
+  t[0] = movt(p[0]);
+  t[1] = movt(p[2]);
+  t[2] = movt(p[1]);
+  t[3] = movt(p[3]);
+}
+
+// MT m-tiles (16 MT pixels from px0) of one step: the loss into lp and, when
+// bwd, this tile's outer products into G.  colx / rowy: coordinate tables.
+template <int H, int MT>
+__device__ __forceinline__ void mma_pass(const FitFrags& F, const FitArgs& A, const float* __restrict__ img,
+                                         const float* colx, const float* rowy, float inv_wd, int px0, float om,
+                                         float s2, bool bwd, int lane, double& lp, FitGrads& G) {
+  const int g = lane >> 2, tq = lane & 3;
+  float x[MT][2], y[MT][2], tg[MT][2][2];
+  bool ok[MT][2];
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int px = px0 + 16 * mt + g + 8 * h;
+      ok[mt][h] = px < A.hw;
+      int pr = int(float(px) * inv_wd), pc = px - pr * A.wd;  // exact after one correction
+      if (pc < 0) {
+        --pr;
+        pc += A.wd;
+      } else if (pc >= A.wd) {
+        ++pr;
+        pc -= A.wd;
+      }
+      if (!ok[mt][h]) pr = pc = 0;
+      x[mt][h] = colx[pc];
+      y[mt][h] = rowy[pr];
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+        tg[mt][h][e] = ok[mt][h] && 2 * tq + e < 3 ? img[3 * px + 2 * tq + e] : 0.0f;
+    }
+  // per-lane unit masks: keep = 1 for real units, one = 1 at the ones column (unit H)
+  float keep[2][2], one[2][2];
+#pragma unroll
+  for (int j = 0; j < 2; ++j)
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int u = 8 * j + 2 * tq + e;
+      keep[j][e] = u < H ? 1.0f : 0.0f;
+      one[j][e] = u == H ? 1.0f : 0.0f;
+    }
+#pragma unroll
+  for (int mt = 0; mt < MT; ++mt) {
+    // layer 0 (FFMA, fragment layout)
+    float v[2][4], c0[2][4];
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int h = e >> 1;
+        const float z = __fadd_rn(fmaf(y[mt][h], F.w0y[j][e & 1], __fmul_rn(x[mt][h], F.w0x[j][e & 1])), F.b0[j][e & 1]);
+        float sn, cs;
+        __sincosf(__fmul_rn(om, z), &sn, &cs);
+        v[j][e] = fmaf(sn, keep[j][e & 1], one[j][e & 1]);
+        c0[j][e] = __fmul_rn(__fmul_rn(om, cs), keep[j][e & 1]);
+      }
+    uint32_t a0h[4], a0l[4];
+    frag_a(v, a0h, a0l);
+    // layer 1
+    float c1[2][4];
+    {
+      float z[2][4] = {};
+#pragma unroll
+      for (int j = 0; j < 2; ++j) mma3(z[j], a0h, a0l, F.w1f[j]);
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          float sn, cs;
+          __sincosf(__fmul_rn(om, __fadd_rn(z[j][e], F.b1[j][e & 1])), &sn, &cs);
+          v[j][e] = fmaf(sn, keep[j][e & 1], one[j][e & 1]);
+          c1[j][e] = __fmul_rn(__fmul_rn(om, cs), keep[j][e & 1]);
+        }
+    }
+    uint32_t a1h[4], a1l[4];
+    frag_a(v, a1h, a1l);
+    // layer 2, residual, loss, d2 = (2 / size) * resid
+    float d2[4];
+    {
+      float o[4] = {};
+      mma3(o, a1h, a1l, F.w2f);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int h = e >> 1;
+        const bool val = ok[mt][h] && 2 * tq + (e & 1) < 3;
+        const float r = __fsub_rn(__fadd_rn(o[e], F.b2[e & 1]), tg[mt][h][e & 1]);
+        if (val) lp += double(r) * double(r);
+        d2[e] = val ? __fmul_rn(s2, r) : 0.0f;
+      }
+    }
+    if (!bwd) continue;
+    // d1 = (d2 W2) * c1: A = d2 (K = output j; columns >= 8 zero)
+    uint32_t d2h[4] = {0u, 0u, 0u, 0u}, d2l[4] = {0u, 0u, 0u, 0u};
+    pack_act<true>(d2[0], d2[1], d2h[0], d2l[0]);
+    pack_act<true>(d2[2], d2[3], d2h[1], d2l[1]);
+    {
+      float q[2][4] = {};
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        mma16816(q[j], d2h, F.w2b[j][0], 0u);
+        mma16816(q[j], d2l, F.w2b[j][0], 0u);
+        mma16816(q[j], d2h, F.w2b[j][1], 0u);
+      }
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) c1[j][e] = __fmul_rn(q[j][e], c1[j][e]);  // c1 := d1
+    }
+    uint32_t d1h[4], d1l[4];
+    frag_a(c1, d1h, d1l);
+    // d0 = (d1 W1) * c0
+    {
+      float r[2][4] = {};
+#pragma unroll
+      for (int j = 0; j < 2; ++j) mma3(r[j], d1h, d1l, F.w1b[j]);
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) c0[j][e] = __fmul_rn(r[j][e], c0[j][e]);  // c0 := d0
+    }
+    // gradient sums over this tile's 16 pixels (bf16 3-pass, K = pixels)
+    {
+      uint32_t th[4], tl[4], bh[4], bl[4];
+      frag_at(d1h, th);  // A = d1^T
+      frag_at(d1l, tl);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {  // B = [a0 | 1]: n-tile j = words 2j, 2j+1
+        bh[i] = movt(a0h[i]);
+        bl[i] = movt(a0l[i]);
+      }
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        mma16816(G.w1[j], th, bh[2 * j], bh[2 * j + 1]);
+        mma16816(G.w1[j], tl, bh[2 * j], bh[2 * j + 1]);
+        mma16816(G.w1[j], th, bl[2 * j], bl[2 * j + 1]);
+      }
+      frag_at(a1h, th);  // A = [a1 | 1]^T, B = d2
+      frag_at(a1l, tl);
+      const uint32_t e0h = movt(d2h[0]), e1h = movt(d2h[1]), e0l = movt(d2l[0]), e1l = movt(d2l[1]);
+      mma16816(G.w2t, th, e0h, e1h);
+      mma16816(G.w2t, tl, e0h, e1h);
+      mma16816(G.w2t, th, e0l, e1l);
+      uint32_t d0h[4], d0l[4];
+      frag_a(c0, d0h, d0l);
+      frag_at(d0h, th);  // A = d0^T, B = [x y 1] of pixels 2tq, 2tq+1 (+8)
+      frag_at(d0l, tl);
+      float xb[4], yb[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int src = 4 * (2 * tq + (i & 1));  // lane holding pixel row 2tq + (i&1) (+8 for i >= 2)
+        xb[i] = __shfl_sync(0xffffffffu, x[mt][i >> 1], src);
+        yb[i] = __shfl_sync(0xffffffffu, y[mt][i >> 1], src);
+      }
+      auto col = [&](int i) { return g == 0 ? xb[i] : (g == 1 ? yb[i] : (g == 2 ? 1.0f : 0.0f)); };
+      uint32_t b0h, b0l, b1h, b1l;
+      pack_act<true>(col(0), col(1), b0h, b0l);
+      pack_act<true>(col(2), col(3), b1h, b1l);
+      mma16816(G.w0, th, b0h, b1h);
+      mma16816(G.w0, tl, b0h, b1h);
+      mma16816(G.w0, th, b0l, b1l);
+    }
+  }
+}
+
+// Fold a warp's step sums into its partial row (canonical order; one owner per entry)
+template <int H>
+__device__ __forceinline__ void fold_grads(const FitGrads& G, float* pw, int lane) {
+  using L = FitLayout<H>;
+  const int g = lane >> 2, tq = lane & 3;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const int r = g + 8 * (e >> 1), cb = 2 * tq + (e & 1);
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int k = 8 * j + cb;
+      if (r < H) {
+        if (k < H) pw[2 * H + r * H + k] += G.w1[j][e];
+        else if (k == H) pw[L::P + H + r] += G.w1[j][e];
+      }
+    }
+    if (cb < 3) {
+      if (r < H) pw[2 * H + H * H + cb * H + r] += G.w2t[e];
+      else if (r == H) pw[L::P + 2 * H + cb] += G.w2t[e];
+    }
+    if (r < H) {
+      if (cb < 2) pw[2 * r + cb] += G.w0[e];
+      else if (cb == 2) pw[L::P + r] += G.w0[e];
+    }
+  }
+}
+
+template <int H, bool ACC, int NPX, bool MMA>
 __global__ void __launch_bounds__(kFitThreads / NPX, 1) fit_kernel(FitArgs A) {
+  static_assert(!MMA || (!ACC && H < 16), "tensor-core pixel pass: MUFU sine, H < 16");
   using L = FitLayout<H>;
   constexpr int NWP = kFitWarps / NPX;         // warps per CTA
   constexpr int NTH = NWP * 32;                // threads per CTA
@@ -354,7 +639,9 @@ __global__ void __launch_bounds__(kFitThreads / NPX, 1) fit_kernel(FitArgs A) {
   float* mk = ve + L::NPAR_PAD;
   float* part = mk + ((L::P + 3) & ~3);
   float* stage = part + NWP * L::NPAR_PAD;
-  double* lossw = reinterpret_cast<double*>(stage + NWP * CPX * kStage);
+  double* lossw = reinterpret_cast<double*>(stage + (MMA ? 0 : NWP * CPX * kStage));
+  float* colx = reinterpret_cast<float*>(lossw + kFitWarps);  // MMA pass: coordinate tables
+  float* rowy = colx + A.wd;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int64_t m = blockIdx.x;
   float* gw = A.w + m * L::P;
@@ -368,7 +655,12 @@ __global__ void __launch_bounds__(kFitThreads / NPX, 1) fit_kernel(FitArgs A) {
     ve[p] = 0.0f;
     if (p < L::P) mk[p] = A.mask[m * L::P + p] ? 1.0f : 0.0f;
   }
+  if constexpr (MMA) {
+    for (int i = tid; i < A.wd; i += NTH) colx[i] = grid_coord(i, A.wd, A.inv_wm1);
+    for (int i = tid; i < A.h; i += NTH) rowy[i] = grid_coord(i, A.h, A.inv_hm1);
+  }
   __syncthreads();
+  const float inv_wd = 1.0f / float(A.wd);
 
   const int HW = A.hw, nchunks = (HW + CPX - 1) / CPX;
   const double scale = 1.0 / (3.0 * double(HW));  // 1.0 / resid.size
@@ -386,6 +678,9 @@ __global__ void __launch_bounds__(kFitThreads / NPX, 1) fit_kernel(FitArgs A) {
     // t == steps: the final forward-only loss (encoder.py:84), except for the
     // loss_and_grad hook (steps == 0 with gradient outputs)
     const bool last = t == A.steps && !(A.grad_w && A.steps == 0);
+    FitFrags F;
+    FitGrads G = {};
+    if constexpr (MMA) load_frags<H>(ws, lane, F);  // this step's weights as MMA B fragments
     // this warp's partial gradient row (canonical order), summed over its chunks
     float* pw = part + warp * L::NPAR_PAD;
     if (!last)
@@ -393,6 +688,13 @@ __global__ void __launch_bounds__(kFitThreads / NPX, 1) fit_kernel(FitArgs A) {
     __syncwarp();
     double lp = 0.0;
     for (int ch = warp; ch < nchunks; ch += NWP) {
+      if constexpr (MMA) {
+        constexpr int MT = 2;  // m-tiles per pass
+#pragma unroll 1
+        for (int q = 0; q < CPX; q += 16 * MT)
+          mma_pass<H, MT>(F, A, img, colx, rowy, inv_wd, ch * CPX + q, om, s2, !last, lane, lp, G);
+        continue;  // the gradient sums stay in G until the end of the step
+      } else {
       float x[NPX], y[NPX], tg[NPX][3];
       bool valid[NPX];
 #pragma unroll
@@ -439,6 +741,7 @@ __global__ void __launch_bounds__(kFitThreads / NPX, 1) fit_kernel(FitArgs A) {
           row[SA0 + H] = 1.0f;
           row[SA1 + H] = 1.0f;
         }
+      }
       }
       __syncwarp();
       const int nq = HW - ch * CPX < CPX ? HW - ch * CPX : CPX;
@@ -508,6 +811,8 @@ __global__ void __launch_bounds__(kFitThreads / NPX, 1) fit_kernel(FitArgs A) {
       }
       __syncwarp();
     }
+    if constexpr (MMA)
+      if (!last) fold_grads<H>(G, pw, lane);
     // loss of this step (weights before the update)
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) lp += __shfl_xor_sync(0xffffffffu, lp, d);
@@ -603,18 +908,20 @@ int fit_arch(const int32_t* dims, int nl, int& H) {
   return RINR_OK;
 }
 
-template <int H, bool ACC, int NPX>
+template <int H, bool ACC, int NPX, bool MMA>
 int launch_fit(const FitArgs& a, cudaStream_t st) {
-  constexpr size_t smem = FitLayout<H>::smem_bytes(NPX);
-  static_assert(smem <= 227 * 1024, "fit kernel shared memory");
+  constexpr size_t smem0 = FitLayout<H>::smem_bytes(NPX, !MMA);
+  static_assert(smem0 <= 227 * 1024, "fit kernel shared memory");
+  const size_t smem = smem0 + (MMA ? sizeof(float) * size_t(a.h + a.wd) : 0);
+  if (smem > 227 * 1024) return set_error(RINR_ERR_UNSUPPORTED, "fit: image too large for the coordinate tables");
   static bool attr = false;
   if (!attr) {
-    if (cudaFuncSetAttribute(fit_kernel<H, ACC, NPX>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) !=
+    if (cudaFuncSetAttribute(fit_kernel<H, ACC, NPX, MMA>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) !=
         cudaSuccess)
       return set_error(RINR_ERR_CUDA, "fit smem attribute");
     attr = true;
   }
-  fit_kernel<H, ACC, NPX><<<unsigned(a.n), kFitThreads / NPX, smem, st>>>(a);
+  fit_kernel<H, ACC, NPX, MMA><<<unsigned(a.n), kFitThreads / NPX, smem, st>>>(a);
   const cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return set_error(RINR_ERR_CUDA, std::string("fit launch: ") + cudaGetErrorString(e));
   return RINR_OK;
@@ -624,7 +931,12 @@ int launch_fit(const FitArgs& a, cudaStream_t st) {
 // serves two pixels (one pixel per thread with 16 warps measured 6% slower)
 template <int H>
 int dispatch_fit(const FitArgs& a, bool acc, cudaStream_t st) {
-  return acc ? launch_fit<H, true, RINR_FIT_NPX>(a, st) : launch_fit<H, false, RINR_FIT_NPX>(a, st);
+  if (acc) return launch_fit<H, true, RINR_FIT_NPX, false>(a, st);
+  // MUFU mode: tensor-core pixel pass (H < 16; RINR_FIT_FFMA builds the fp32 FFMA pass instead)
+#ifndef RINR_FIT_FFMA
+  if constexpr (H < 16) return launch_fit<H, false, RINR_FIT_NPX, true>(a, st);
+#endif
+  return launch_fit<H, false, RINR_FIT_NPX, false>(a, st);
 }
 
 template <int H, bool ACC>
