@@ -11,9 +11,11 @@
  *
  * One CTA fits one image.  All `steps` Adam steps of a round run inside one
  * launch, with weights, moments and masks in shared memory.  The arithmetic
- * is fp32 like the reference:
- *   * forward / backward run per pixel (FFMA; sine on MUFU or accurate sinf);
- *   * the gradient sums over pixels stage per-warp outer products in shared memory;
+ * follows the reference's fp32 algorithm:
+ *   * RINR_SIN_ACCURATE: forward / backward per pixel in fp32 FFMA with
+ *     accurate sinf, gradient sums in 3xTF32 (fp32-accurate);
+ *   * RINR_SIN_MUFU (H < 16): the matrix products and gradient sums on
+ *     mma.sync in bf16 3-pass (about 2^-16 relative per product), sines on MUFU;
  *   * the Adam update reproduces numpy's f32 operation order exactly.
  * Gradients match net.loss_and_grad to summation order (tests state
  * the tolerance); trajectories therefore agree statistically, not bitwise.

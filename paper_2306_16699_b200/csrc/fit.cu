@@ -4,17 +4,20 @@
 // round inside one launch.
 //
 // Architecture (2, H, H, 3), 8 <= H <= 16, omega from the record.  Per step:
-//   1. thread = pixel: forward (FFMA + sin/cos) and backward (deltas) in
-//      fp32 registers, the loss accumulated in f64 (resid.astype(f64)**2);
-//   2. each warp stages its 32 pixels' (a0, a1, d0, d1, d2, x, y) in shared
-//      memory, then the lanes reduce the outer products over those pixels in
-//      one uniform instruction stream.  Lanes 0..15 own W1[o][0..7] plus
-//      W0[o][:] / b0 / b1; lanes 16..31 own W1[o][8..] plus W2[:][o] (and b2),
-//      with o = lane % 16;
-//   3. cross-warp sums in shared memory, then the Adam update in numpy's f32
+//   1. forward + backward of every pixel, the loss accumulated in f64
+//      (resid.astype(f64)**2), and the gradient sums over pixels:
+//        * MUFU sine, H < 16 (mma_pass): register-resident mma.sync bf16
+//          3-pass chains in fragment layout, gradient sums accumulated in MMA
+//          registers through movmatrix transposes; 2 CTAs per SM;
+//        * accurate sine or H = 16 (pixel_pass): fp32 FFMA, one thread per
+//          pixel pair, rows staged in shared memory and reduced by 3xTF32
+//          mma.m16n8k8 (tc_reduce) or a lane-tiled FFMA loop (H = 16);
+//   2. cross-warp sums in shared memory, then the Adam update in numpy's f32
 //      operation order, with the mask re-applied.
-// Shared memory holds the weights (compute copy, padded rows), Adam moments,
-// masks, per-warp partial gradients and the staging tiles: about 180 KB, one CTA per SM.
+// Shared memory holds the weights (compute copy, padded rows, plus a
+// transposed W1), Adam moments, masks, per-warp partial gradients and either
+// the staging tiles (FFMA pass, ~180 KB) or the per-warp B fragments and
+// coordinate tables (MMA pass, ~42 KB).
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -35,6 +38,7 @@ namespace {
 #endif
 constexpr int kFitWarps = 16;
 constexpr int kFitThreads = kFitWarps * 32;
+constexpr int kFragGroups = 6;  // uint4 B-fragment groups per lane (MMA pass)
 constexpr int kStage = 76;  // floats per staged pixel (stride 76: conflict-free STS.128)
 // staged pixel: a0 [0,16) a1 [16,32) d1 [32,48) d0 [48,64) d2 [64,68) (x, y) [68,70)
 constexpr int SA0 = 0, SA1 = 16, SD1 = 32, SD0 = 48, SD2 = 64, SXY = 68;
@@ -74,7 +78,7 @@ struct FitLayout {
   static constexpr size_t smem_bytes(int npx, bool stage = true) {
     return sizeof(float) * (size_t(WS) + 2 * NPAR_PAD + ((P + 3) & ~3) + size_t(kFitWarps / npx) * NPAR_PAD +
                             (stage ? size_t(kFitWarps / npx) * 32 * npx * kStage : 0)) +
-           sizeof(double) * kFitWarps;
+           sizeof(double) * kFitWarps + (stage ? 0 : sizeof(uint32_t) * 4 * 32 * kFragGroups * (kFitWarps / npx));
   }
 };
 
@@ -355,29 +359,43 @@ __device__ __forceinline__ void tc_reduce(const float* st, int rows, float* pw, 
 // Layer 0 (K = 2) is FFMA in the same fragment layout.  C-fragment element e
 // of n-tile j: pixel row g + 8(e >> 1), unit 8j + 2tq + (e & 1).
 // ---------------------------------------------------------------------------
+// B fragments live in a per-warp shared block (6 uint4 groups x 32 lanes,
+// read with one LDS.128 right before each use, keeping ~24 registers free):
+//   group 0/1: forward W1 n-tile 0/1, B[k][n] = W1[n][k], {b0 hi, b1 hi, b0 lo, b1 lo}
+//   group 2/3: backward W1 n-tile 0/1, B[o][k] = W1[o][k]
+//   group 4:   forward W2, B[k][j] = W2[j][k] (3 valid columns)
+//   group 5:   backward W2 n-tiles 0/1, B[j][o] = W2[j][o] (K = 3 valid): {hi0, lo0, hi1, lo1}
 struct FitFrags {
-  uint32_t w1f[2][4];  // forward B[k][n] = W1[n][k]: {b0 hi, b1 hi, b0 lo, b1 lo} per n-tile
-  uint32_t w1b[2][4];  // backward B[o][k] = W1[o][k]
-  uint32_t w2f[4];     // forward B[k][j] = W2[j][k] (3 valid columns)
-  uint32_t w2b[2][2];  // backward B[j][o] = W2[j][o] (K = 3 valid): {hi, lo}
   float w0x[2][2], w0y[2][2], b0[2][2], b1[2][2], b2[2];  // this lane's units / outputs
 };
 
+__device__ __forceinline__ uint4 frag_ld(const uint4* p) {
+  uint4 v;
+  asm volatile("ld.volatile.shared.v4.u32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(static_cast<unsigned>(__cvta_generic_to_shared(p))));
+  return v;
+}
+
 template <int H>
-__device__ __forceinline__ void load_frags(const float* ws, int lane, FitFrags& F) {
+__device__ __forceinline__ void load_frags(const float* ws, int lane, FitFrags& F, uint4* fq) {
   using L = FitLayout<H>;
   const int g = lane >> 2, tq = lane & 3;
   // W1 rows are zero padded to 16 x 16, W2 to 4 x 16 (ws is zeroed at start)
   auto W1 = [&](int o, int k) { return ws[L::W1S + 16 * o + k]; };
   auto W2 = [&](int j, int k) { return j < 3 ? ws[L::W2S + 16 * j + k] : 0.0f; };
+  uint32_t w2b[4];
 #pragma unroll
   for (int j = 0; j < 2; ++j) {
     const int n = 8 * j + g;
-    pack_act<true>(W1(n, 2 * tq), W1(n, 2 * tq + 1), F.w1f[j][0], F.w1f[j][2]);
-    pack_act<true>(W1(n, 2 * tq + 8), W1(n, 2 * tq + 9), F.w1f[j][1], F.w1f[j][3]);
-    pack_act<true>(W1(2 * tq, n), W1(2 * tq + 1, n), F.w1b[j][0], F.w1b[j][2]);
-    pack_act<true>(W1(2 * tq + 8, n), W1(2 * tq + 9, n), F.w1b[j][1], F.w1b[j][3]);
-    pack_act<true>(W2(2 * tq, n), W2(2 * tq + 1, n), F.w2b[j][0], F.w2b[j][1]);
+    uint32_t f[4], b[4];
+    pack_act<true>(W1(n, 2 * tq), W1(n, 2 * tq + 1), f[0], f[2]);
+    pack_act<true>(W1(n, 2 * tq + 8), W1(n, 2 * tq + 9), f[1], f[3]);
+    pack_act<true>(W1(2 * tq, n), W1(2 * tq + 1, n), b[0], b[2]);
+    pack_act<true>(W1(2 * tq + 8, n), W1(2 * tq + 9, n), b[1], b[3]);
+    pack_act<true>(W2(2 * tq, n), W2(2 * tq + 1, n), w2b[2 * j], w2b[2 * j + 1]);
+    fq[32 * j] = make_uint4(f[0], f[1], f[2], f[3]);
+    fq[32 * (2 + j)] = make_uint4(b[0], b[1], b[2], b[3]);
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
       const int u = 8 * j + 2 * tq + e;
@@ -387,8 +405,11 @@ __device__ __forceinline__ void load_frags(const float* ws, int lane, FitFrags& 
       F.b1[j][e] = ws[L::B1S + u];
     }
   }
-  pack_act<true>(W2(g, 2 * tq), W2(g, 2 * tq + 1), F.w2f[0], F.w2f[2]);
-  pack_act<true>(W2(g, 2 * tq + 8), W2(g, 2 * tq + 9), F.w2f[1], F.w2f[3]);
+  uint32_t f[4];
+  pack_act<true>(W2(g, 2 * tq), W2(g, 2 * tq + 1), f[0], f[2]);
+  pack_act<true>(W2(g, 2 * tq + 8), W2(g, 2 * tq + 9), f[1], f[3]);
+  fq[32 * 4] = make_uint4(f[0], f[1], f[2], f[3]);
+  fq[32 * 5] = make_uint4(w2b[0], w2b[1], w2b[2], w2b[3]);
   F.b2[0] = ws[L::B2S + 2 * tq];  // zero beyond the 3 outputs
   F.b2[1] = ws[L::B2S + 2 * tq + 1];
 }
@@ -402,11 +423,10 @@ __device__ __forceinline__ void frag_a(const float (&v)[2][4], uint32_t (&hi)[4]
 }
 
 // c += A * B in three bf16 passes (B given as {b0 hi, b1 hi, b0 lo, b1 lo})
-__device__ __forceinline__ void mma3(float (&c)[4], const uint32_t (&ah)[4], const uint32_t (&al)[4],
-                                     const uint32_t (&b)[4]) {
-  mma16816(c, ah, b[0], b[1]);
-  mma16816(c, al, b[0], b[1]);
-  mma16816(c, ah, b[2], b[3]);
+__device__ __forceinline__ void mma3(float (&c)[4], const uint32_t (&ah)[4], const uint32_t (&al)[4], uint4 b) {
+  mma16816(c, ah, b.x, b.y);
+  mma16816(c, al, b.x, b.y);
+  mma16816(c, ah, b.z, b.w);
 }
 
 // Transpose of an 8 x 8 bf16 block held one row per 4 lanes (C / A fragment
@@ -438,7 +458,7 @@ __device__ __forceinline__ void frag_at(const uint32_t (&p)[4], uint32_t (&t)[4]
 // MT m-tiles (16 MT pixels from px0) of one step: the loss into lp and, when
 // bwd, this tile's outer products into G.  colx / rowy: coordinate tables.
 template <int H, int MT>
-__device__ __forceinline__ void mma_pass(const FitFrags& F, const FitArgs& A, const float* __restrict__ img,
+__device__ __forceinline__ void mma_pass(const FitFrags& F, const uint4* fq, const FitArgs& A, const float* __restrict__ img,
                                          const float* colx, const float* rowy, float inv_wd, int px0, float om,
                                          float s2, bool bwd, int lane, double& lp, FitGrads& G) {
   const int g = lane >> 2, tq = lane & 3;
@@ -466,7 +486,7 @@ __device__ __forceinline__ void mma_pass(const FitFrags& F, const FitArgs& A, co
         tg[mt][h][e] = ok[mt][h] && 2 * tq + e < 3 ? img[3 * px + 2 * tq + e] : 0.0f;
     }
   // per-lane unit masks: keep = 1 for real units, one = 1 at the ones column (unit H)
-  float keep[2][2], one[2][2];
+  float keep[2][2], one[2][2], omk[2][2];  // omk = omega for real units, 0 for pads
 #pragma unroll
   for (int j = 0; j < 2; ++j)
 #pragma unroll
@@ -474,6 +494,7 @@ __device__ __forceinline__ void mma_pass(const FitFrags& F, const FitArgs& A, co
       const int u = 8 * j + 2 * tq + e;
       keep[j][e] = u < H ? 1.0f : 0.0f;
       one[j][e] = u == H ? 1.0f : 0.0f;
+      omk[j][e] = u < H ? om : 0.0f;
     }
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt) {
@@ -488,7 +509,7 @@ __device__ __forceinline__ void mma_pass(const FitFrags& F, const FitArgs& A, co
         float sn, cs;
         __sincosf(__fmul_rn(om, z), &sn, &cs);
         v[j][e] = fmaf(sn, keep[j][e & 1], one[j][e & 1]);
-        c0[j][e] = __fmul_rn(__fmul_rn(om, cs), keep[j][e & 1]);
+        c0[j][e] = __fmul_rn(omk[j][e & 1], cs);
       }
     uint32_t a0h[4], a0l[4];
     frag_a(v, a0h, a0l);
@@ -497,7 +518,7 @@ __device__ __forceinline__ void mma_pass(const FitFrags& F, const FitArgs& A, co
     {
       float z[2][4] = {};
 #pragma unroll
-      for (int j = 0; j < 2; ++j) mma3(z[j], a0h, a0l, F.w1f[j]);
+      for (int j = 0; j < 2; ++j) mma3(z[j], a0h, a0l, frag_ld(fq + 32 * j));
 #pragma unroll
       for (int j = 0; j < 2; ++j)
 #pragma unroll
@@ -505,7 +526,7 @@ __device__ __forceinline__ void mma_pass(const FitFrags& F, const FitArgs& A, co
           float sn, cs;
           __sincosf(__fmul_rn(om, __fadd_rn(z[j][e], F.b1[j][e & 1])), &sn, &cs);
           v[j][e] = fmaf(sn, keep[j][e & 1], one[j][e & 1]);
-          c1[j][e] = __fmul_rn(__fmul_rn(om, cs), keep[j][e & 1]);
+          c1[j][e] = __fmul_rn(omk[j][e & 1], cs);
         }
     }
     uint32_t a1h[4], a1l[4];
@@ -514,7 +535,7 @@ __device__ __forceinline__ void mma_pass(const FitFrags& F, const FitArgs& A, co
     float d2[4];
     {
       float o[4] = {};
-      mma3(o, a1h, a1l, F.w2f);
+      mma3(o, a1h, a1l, frag_ld(fq + 32 * 4));
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int h = e >> 1;
@@ -531,12 +552,13 @@ __device__ __forceinline__ void mma_pass(const FitFrags& F, const FitArgs& A, co
     pack_act<true>(d2[2], d2[3], d2h[1], d2l[1]);
     {
       float q[2][4] = {};
-#pragma unroll
-      for (int j = 0; j < 2; ++j) {
-        mma16816(q[j], d2h, F.w2b[j][0], 0u);
-        mma16816(q[j], d2l, F.w2b[j][0], 0u);
-        mma16816(q[j], d2h, F.w2b[j][1], 0u);
-      }
+      const uint4 w = frag_ld(fq + 32 * 5);
+      mma16816(q[0], d2h, w.x, 0u);
+      mma16816(q[1], d2h, w.z, 0u);
+      mma16816(q[0], d2l, w.x, 0u);
+      mma16816(q[1], d2l, w.z, 0u);
+      mma16816(q[0], d2h, w.y, 0u);
+      mma16816(q[1], d2h, w.w, 0u);
 #pragma unroll
       for (int j = 0; j < 2; ++j)
 #pragma unroll
@@ -548,7 +570,7 @@ __device__ __forceinline__ void mma_pass(const FitFrags& F, const FitArgs& A, co
     {
       float r[2][4] = {};
 #pragma unroll
-      for (int j = 0; j < 2; ++j) mma3(r[j], d1h, d1l, F.w1b[j]);
+      for (int j = 0; j < 2; ++j) mma3(r[j], d1h, d1l, frag_ld(fq + 32 * (2 + j)));
 #pragma unroll
       for (int j = 0; j < 2; ++j)
 #pragma unroll
@@ -625,8 +647,14 @@ __device__ __forceinline__ void fold_grads(const FitGrads& G, float* pw, int lan
   }
 }
 
+#ifndef RINR_FIT_MINB
+#define RINR_FIT_MINB 2  // CTAs per SM the MMA pass is compiled for (128 registers)
+#endif
+#ifndef RINR_FIT_MT
+#define RINR_FIT_MT 2  // m-tiles per MMA pass
+#endif
 template <int H, bool ACC, int NPX, bool MMA>
-__global__ void __launch_bounds__(kFitThreads / NPX, 1) fit_kernel(FitArgs A) {
+__global__ void __launch_bounds__(kFitThreads / NPX, MMA ? RINR_FIT_MINB : 1) fit_kernel(FitArgs A) {
   static_assert(!MMA || (!ACC && H < 16), "tensor-core pixel pass: MUFU sine, H < 16");
   using L = FitLayout<H>;
   constexpr int NWP = kFitWarps / NPX;         // warps per CTA
@@ -640,9 +668,10 @@ __global__ void __launch_bounds__(kFitThreads / NPX, 1) fit_kernel(FitArgs A) {
   float* part = mk + ((L::P + 3) & ~3);
   float* stage = part + NWP * L::NPAR_PAD;
   double* lossw = reinterpret_cast<double*>(stage + (MMA ? 0 : NWP * CPX * kStage));
-  float* colx = reinterpret_cast<float*>(lossw + kFitWarps);  // MMA pass: coordinate tables
-  float* rowy = colx + A.wd;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  uint4* frg = reinterpret_cast<uint4*>(lossw + kFitWarps) + warp * kFragGroups * 32 + lane;  // MMA pass
+  float* colx = reinterpret_cast<float*>(reinterpret_cast<uint4*>(lossw + kFitWarps) + NWP * kFragGroups * 32);
+  float* rowy = colx + A.wd;
   const int64_t m = blockIdx.x;
   float* gw = A.w + m * L::P;
   float* gb = A.b + m * L::PB;
@@ -680,7 +709,10 @@ __global__ void __launch_bounds__(kFitThreads / NPX, 1) fit_kernel(FitArgs A) {
     const bool last = t == A.steps && !(A.grad_w && A.steps == 0);
     FitFrags F;
     FitGrads G = {};
-    if constexpr (MMA) load_frags<H>(ws, lane, F);  // this step's weights as MMA B fragments
+    if constexpr (MMA) {
+      load_frags<H>(ws, lane, F, frg);  // this step's weights as MMA B fragments
+      __syncwarp();
+    }
     // this warp's partial gradient row (canonical order), summed over its chunks
     float* pw = part + warp * L::NPAR_PAD;
     if (!last)
@@ -689,10 +721,10 @@ __global__ void __launch_bounds__(kFitThreads / NPX, 1) fit_kernel(FitArgs A) {
     double lp = 0.0;
     for (int ch = warp; ch < nchunks; ch += NWP) {
       if constexpr (MMA) {
-        constexpr int MT = 2;  // m-tiles per pass
+        constexpr int MT = RINR_FIT_MT;
 #pragma unroll 1
         for (int q = 0; q < CPX; q += 16 * MT)
-          mma_pass<H, MT>(F, A, img, colx, rowy, inv_wd, ch * CPX + q, om, s2, !last, lane, lp, G);
+          mma_pass<H, MT>(F, frg, A, img, colx, rowy, inv_wd, ch * CPX + q, om, s2, !last, lane, lp, G);
         continue;  // the gradient sums stay in G until the end of the step
       } else {
       float x[NPX], y[NPX], tg[NPX][3];

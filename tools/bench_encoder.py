@@ -5,10 +5,11 @@ trainer's algorithm on the host cores (the oracle port of encoder._train).
 
 Lines (JSON):
   * fit_step: images x Adam steps per second for `--steps` steps of round 1
-    (CUDA events), with an FFMA roofline over algorithmic FLOPs:
+    (CUDA events), with an FFMA-equivalent roofline over algorithmic FLOPs:
     per pixel per step forward 2*(2H + H^2 + 3H), backward deltas 2*(3H + H^2),
     weight gradients 2*(2H + H^2 + 3H) (H = 15: 1740 FLOP), against the FFMA
-    peak measured by the diag microbenchmark in this process;
+    peak measured by the diag microbenchmark in this process, and the MUFU
+    fraction (60 sin/cos per pixel-step against the measured MUFU.SIN rate);
   * fit_full (with --full): wall-clock images/s of the whole default pipeline
     (5,000 + 10,000 + 10,000 steps, two prunes, four PSNR renders).
 The CPU baseline times the oracle's numpy loss_and_grad + Adam per image on
@@ -57,9 +58,12 @@ def cpu_rate(imgs, steps):
     return cores / per_step, cores, wall, per_step
 
 
-def ffma_peak():
+def peaks():
     import bench
-    return bench.measure_peaks(torch, N.lib())["ffma_flop_per_s"]
+    return bench.measure_peaks(torch, N.lib())
+
+
+MUFU_PX = 2 * 2 * H  # sin + cos per hidden unit of both sine layers (60 MUFU ops per pixel-step)
 
 
 def main():
@@ -85,8 +89,10 @@ def main():
     torch.cuda.synchronize()
     dt = e0.elapsed_time(e1) * 1e-3
     rate = n * a.steps / dt
-    peak = ffma_peak()
+    pk = peaks()
+    peak = pk["ffma_flop_per_s"]
     achieved = rate * 32 * 32 * FLOP_PX
+    mufu = rate * 32 * 32 * MUFU_PX
     cpu = None
     if not a.no_cpu:
         r, cores, wall, per_step = cpu_rate(imgs, 40)
@@ -97,7 +103,11 @@ def main():
     line = {"metric": "encoder image-steps/sec (full-batch Adam on 32x32, arch (2,15,15,3))", "value": rate,
             "unit": "image-steps/s", "ms": dt * 1e3, "config": {"images": n, "steps": a.steps, "h": 32, "w": 32},
             "roofline": {"bound": "ffma", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "flop_per_pixel_step": FLOP_PX},
+                         "frac": achieved / peak, "flop_per_pixel_step": FLOP_PX,
+                         "note": "algorithmic FLOPs against the FP32 FFMA peak; in MUFU mode the products run "
+                                 "as bf16 3-pass mma.sync, so this is an equivalent-throughput figure"},
+            "roofline_mufu": {"bound": "mufu", "achieved": mufu / 1e12, "peak": pk["mufu_sin_per_s"] / 1e12,
+                              "unit": "T op/s", "frac": mufu / pk["mufu_sin_per_s"], "ops_per_pixel_step": MUFU_PX},
             "cpu_baseline": cpu, "diverged": int((status != 0).sum()), "gpu_launches": 1}
     print(json.dumps(line), flush=True)
     if a.full:
