@@ -39,6 +39,7 @@ namespace {
 constexpr int kFitWarps = 16;
 constexpr int kFitThreads = kFitWarps * 32;
 constexpr int kFragGroups = 6;  // uint4 B-fragment groups per lane (MMA pass)
+constexpr int kPixTable = 2048;  // MMA pass: per-pixel coordinate / target tables up to this many pixels
 constexpr int kStage = 76;  // floats per staged pixel (stride 76: conflict-free STS.128)
 // staged pixel: a0 [0,16) a1 [16,32) d1 [32,48) d0 [48,64) d2 [64,68) (x, y) [68,70)
 constexpr int SA0 = 0, SA1 = 16, SD1 = 32, SD0 = 48, SD2 = 64, SXY = 68;
@@ -378,7 +379,9 @@ __device__ __forceinline__ uint4 frag_ld(const uint4* p) {
 }
 
 template <int H>
-__device__ __forceinline__ void load_frags(const float* ws, int lane, FitFrags& F, uint4* fq) {
+// The forward fragments carry omega (z' = omega z straight into the sine):
+// layer 0 and 1 weights / biases are pre-multiplied, the backward ones are not.
+__device__ __forceinline__ void load_frags(const float* ws, int lane, float om, FitFrags& F, uint4* fq) {
   using L = FitLayout<H>;
   const int g = lane >> 2, tq = lane & 3;
   // W1 rows are zero padded to 16 x 16, W2 to 4 x 16 (ws is zeroed at start)
@@ -389,8 +392,8 @@ __device__ __forceinline__ void load_frags(const float* ws, int lane, FitFrags& 
   for (int j = 0; j < 2; ++j) {
     const int n = 8 * j + g;
     uint32_t f[4], b[4];
-    pack_act<true>(W1(n, 2 * tq), W1(n, 2 * tq + 1), f[0], f[2]);
-    pack_act<true>(W1(n, 2 * tq + 8), W1(n, 2 * tq + 9), f[1], f[3]);
+    pack_act<true>(om * W1(n, 2 * tq), om * W1(n, 2 * tq + 1), f[0], f[2]);
+    pack_act<true>(om * W1(n, 2 * tq + 8), om * W1(n, 2 * tq + 9), f[1], f[3]);
     pack_act<true>(W1(2 * tq, n), W1(2 * tq + 1, n), b[0], b[2]);
     pack_act<true>(W1(2 * tq + 8, n), W1(2 * tq + 9, n), b[1], b[3]);
     pack_act<true>(W2(2 * tq, n), W2(2 * tq + 1, n), w2b[2 * j], w2b[2 * j + 1]);
@@ -399,10 +402,10 @@ __device__ __forceinline__ void load_frags(const float* ws, int lane, FitFrags& 
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
       const int u = 8 * j + 2 * tq + e;
-      F.w0x[j][e] = ws[L::W0S + 2 * u];
-      F.w0y[j][e] = ws[L::W0S + 2 * u + 1];
-      F.b0[j][e] = ws[L::B0S + u];
-      F.b1[j][e] = ws[L::B1S + u];
+      F.w0x[j][e] = om * ws[L::W0S + 2 * u];
+      F.w0y[j][e] = om * ws[L::W0S + 2 * u + 1];
+      F.b0[j][e] = om * ws[L::B0S + u];
+      F.b1[j][e] = om * ws[L::B1S + u];
     }
   }
   uint32_t f[4];
@@ -456,10 +459,12 @@ __device__ __forceinline__ void frag_at(const uint32_t (&p)[4], uint32_t (&t)[4]
 }
 
 // MT m-tiles (16 MT pixels from px0) of one step: the loss into lp and, when
-// bwd, this tile's outer products into G.  colx / rowy: coordinate tables.
+// bwd, this tile's outer products into G.  xyt / tgt: per-pixel coordinate
+// and target tables (images up to kPixTable pixels), else colx / rowy.
 template <int H, int MT>
 __device__ __forceinline__ void mma_pass(const FitFrags& F, const uint4* fq, const FitArgs& A, const float* __restrict__ img,
-                                         const float* colx, const float* rowy, float inv_wd, int px0, float om,
+                                         const float2* xyt, const float4* tgt, const float* colx,
+                                         const float* rowy, float inv_wd, int px0, float om,
                                          float s2, bool bwd, int lane, double& lp, FitGrads& G) {
   const int g = lane >> 2, tq = lane & 3;
   float x[MT][2], y[MT][2], tg[MT][2][2];
@@ -470,6 +475,15 @@ __device__ __forceinline__ void mma_pass(const FitFrags& F, const uint4* fq, con
     for (int h = 0; h < 2; ++h) {
       const int px = px0 + 16 * mt + g + 8 * h;
       ok[mt][h] = px < A.hw;
+      if (xyt) {
+        const float2 c = ok[mt][h] ? xyt[px] : make_float2(0.0f, 0.0f);
+        const float2 t = ok[mt][h] && tq < 2 ? reinterpret_cast<const float2*>(tgt + px)[tq] : make_float2(0.0f, 0.0f);
+        x[mt][h] = c.x;
+        y[mt][h] = c.y;
+        tg[mt][h][0] = t.x;
+        tg[mt][h][1] = t.y;
+        continue;
+      }
       int pr = int(float(px) * inv_wd), pc = px - pr * A.wd;  // exact after one correction
       if (pc < 0) {
         --pr;
@@ -507,7 +521,7 @@ __device__ __forceinline__ void mma_pass(const FitFrags& F, const uint4* fq, con
         const int h = e >> 1;
         const float z = __fadd_rn(fmaf(y[mt][h], F.w0y[j][e & 1], __fmul_rn(x[mt][h], F.w0x[j][e & 1])), F.b0[j][e & 1]);
         float sn, cs;
-        __sincosf(__fmul_rn(om, z), &sn, &cs);
+        __sincosf(z, &sn, &cs);  // z already carries omega
         v[j][e] = fmaf(sn, keep[j][e & 1], one[j][e & 1]);
         c0[j][e] = __fmul_rn(omk[j][e & 1], cs);
       }
@@ -524,7 +538,7 @@ __device__ __forceinline__ void mma_pass(const FitFrags& F, const uint4* fq, con
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           float sn, cs;
-          __sincosf(__fmul_rn(om, __fadd_rn(z[j][e], F.b1[j][e & 1])), &sn, &cs);
+          __sincosf(__fadd_rn(z[j][e], F.b1[j][e & 1]), &sn, &cs);
           v[j][e] = fmaf(sn, keep[j][e & 1], one[j][e & 1]);
           c1[j][e] = __fmul_rn(omk[j][e & 1], cs);
         }
@@ -670,7 +684,12 @@ __global__ void __launch_bounds__(kFitThreads / NPX, MMA ? RINR_FIT_MINB : 1) fi
   double* lossw = reinterpret_cast<double*>(stage + (MMA ? 0 : NWP * CPX * kStage));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   uint4* frg = reinterpret_cast<uint4*>(lossw + kFitWarps) + warp * kFragGroups * 32 + lane;  // MMA pass
-  float* colx = reinterpret_cast<float*>(reinterpret_cast<uint4*>(lossw + kFitWarps) + NWP * kFragGroups * 32);
+  // MMA pass tables: per-pixel (x, y) and (r, g, b, 0) when hw <= kPixTable, else per-axis coordinates
+  char* tab = reinterpret_cast<char*>(reinterpret_cast<uint4*>(lossw + kFitWarps) + NWP * kFragGroups * 32);
+  const bool pixtab = A.hw <= kPixTable;
+  float2* xyt = pixtab ? reinterpret_cast<float2*>(tab) : nullptr;
+  float4* tgt = pixtab ? reinterpret_cast<float4*>(tab + ((size_t(A.hw) * 8 + 15) & ~size_t(15))) : nullptr;
+  float* colx = reinterpret_cast<float*>(tab);
   float* rowy = colx + A.wd;
   const int64_t m = blockIdx.x;
   float* gw = A.w + m * L::P;
@@ -685,8 +704,17 @@ __global__ void __launch_bounds__(kFitThreads / NPX, MMA ? RINR_FIT_MINB : 1) fi
     if (p < L::P) mk[p] = A.mask[m * L::P + p] ? 1.0f : 0.0f;
   }
   if constexpr (MMA) {
-    for (int i = tid; i < A.wd; i += NTH) colx[i] = grid_coord(i, A.wd, A.inv_wm1);
-    for (int i = tid; i < A.h; i += NTH) rowy[i] = grid_coord(i, A.h, A.inv_hm1);
+    if (pixtab) {
+      const float* im = A.images + m * int64_t(A.hw) * 3;
+      for (int i = tid; i < A.hw; i += NTH) {
+        const int r = i / A.wd, c = i - r * A.wd;
+        xyt[i] = make_float2(grid_coord(c, A.wd, A.inv_wm1), grid_coord(r, A.h, A.inv_hm1));
+        tgt[i] = make_float4(im[3 * i], im[3 * i + 1], im[3 * i + 2], 0.0f);
+      }
+    } else {
+      for (int i = tid; i < A.wd; i += NTH) colx[i] = grid_coord(i, A.wd, A.inv_wm1);
+      for (int i = tid; i < A.h; i += NTH) rowy[i] = grid_coord(i, A.h, A.inv_hm1);
+    }
   }
   __syncthreads();
   const float inv_wd = 1.0f / float(A.wd);
@@ -710,7 +738,7 @@ __global__ void __launch_bounds__(kFitThreads / NPX, MMA ? RINR_FIT_MINB : 1) fi
     FitFrags F;
     FitGrads G = {};
     if constexpr (MMA) {
-      load_frags<H>(ws, lane, F, frg);  // this step's weights as MMA B fragments
+      load_frags<H>(ws, lane, om, F, frg);  // this step's weights as MMA B fragments
       __syncwarp();
     }
     // this warp's partial gradient row (canonical order), summed over its chunks
@@ -724,7 +752,7 @@ __global__ void __launch_bounds__(kFitThreads / NPX, MMA ? RINR_FIT_MINB : 1) fi
         constexpr int MT = RINR_FIT_MT;
 #pragma unroll 1
         for (int q = 0; q < CPX; q += 16 * MT)
-          mma_pass<H, MT>(F, frg, A, img, colx, rowy, inv_wd, ch * CPX + q, om, s2, !last, lane, lp, G);
+          mma_pass<H, MT>(F, frg, A, img, xyt, tgt, colx, rowy, inv_wd, ch * CPX + q, om, s2, !last, lane, lp, G);
         continue;  // the gradient sums stay in G until the end of the step
       } else {
       float x[NPX], y[NPX], tg[NPX][3];
@@ -944,7 +972,9 @@ template <int H, bool ACC, int NPX, bool MMA>
 int launch_fit(const FitArgs& a, cudaStream_t st) {
   constexpr size_t smem0 = FitLayout<H>::smem_bytes(NPX, !MMA);
   static_assert(smem0 <= 227 * 1024, "fit kernel shared memory");
-  const size_t smem = smem0 + (MMA ? sizeof(float) * size_t(a.h + a.wd) : 0);
+  const size_t tabs = a.hw <= kPixTable ? ((size_t(a.hw) * 8 + 15) & ~size_t(15)) + size_t(a.hw) * 16
+                                        : sizeof(float) * size_t(a.h + a.wd);
+  const size_t smem = smem0 + (MMA ? tabs : 0);
   if (smem > 227 * 1024) return set_error(RINR_ERR_UNSUPPORTED, "fit: image too large for the coordinate tables");
   static bool attr = false;
   if (!attr) {

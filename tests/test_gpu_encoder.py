@@ -146,3 +146,27 @@ def test_widths_vs_oracle(E, H):
         assert np.linalg.norm(a - b) <= 1e-4 * np.linalg.norm(b) + 1e-12
     curves, status = E.train_batch(dm, img, 5e-4, 30)
     assert not status.any() and np.isfinite(curves[~np.isnan(curves)]).all()
+
+
+@pytest.mark.parametrize("H,h,w", [(8, 12, 20), (11, 13, 7), (15, 32, 32), (15, 50, 44), (13, 1, 37), (14, 45, 46)])
+def test_mma_pass_vs_oracle(E, H, h, w):
+    """The MUFU-mode tensor-core pass (bf16 3-pass products, movmatrix
+    gradient sums): loss and gradients vs the oracle at the MUFU bar (2e-3)
+    for several widths, ragged sizes (partial 16-pixel tiles) and both pixel
+    table modes (<= 2048 pixels cached per CTA; 50x44 and 45x46 use the
+    per-axis coordinate path)."""
+    from oracle import rinr_oracle as O
+    from transforms_common import cat, smooth_images
+    dims = (2, H, H, 3)
+    x = smooth_images(2, h, w, seed=H + h)
+    dm = E.init_batch(E.Architecture(dims), [H, H + 7], h, w)
+    loss, gw, gb = E.loss_and_grad_batch(dm, torch.from_numpy(x).cuda(), "mufu")
+    coords = O.coordinate_grid(h, w)
+    for i in range(2):
+        ws, bs, ms = O.init_model(dims, [H, H + 7][i])
+        ref_loss, gws, gbs = O.loss_and_grad(ws, bs, ms, 30.0, coords, x[i].reshape(-1, 3))
+        assert abs(loss[i].item() - ref_loss) <= 2e-3 * ref_loss, (H, h, w)
+        a, b = gw[i].cpu().numpy(), cat(gws)
+        assert np.linalg.norm(a - b) <= 2e-3 * np.linalg.norm(b), (H, h, w)
+        a, b = gb[i].cpu().numpy(), cat(gbs)
+        assert np.linalg.norm(a - b) <= 2e-3 * np.linalg.norm(b) + 1e-12, (H, h, w)
