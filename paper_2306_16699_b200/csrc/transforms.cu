@@ -368,6 +368,89 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) prune_warp_kernel(TArch A, 
   if (lane == 0) status[m] = RINR_OK;
 }
 
+// Global-scope prune of one small model (P <= 32 KPL) per warp with the keys
+// in registers, interleaved (key j of a lane is entry 32 j + lane, so global
+// loads and stores are coalesced): the same bisection for T, with per-lane
+// counts and one REDUX per step, then ties ranked in index order by ballots.
+template <int KPL>
+__global__ void __launch_bounds__(kWarpsPerCta * 32) prune_warp_reg_kernel(TArch A, int64_t n, float* __restrict__ w,
+                                                                          uint8_t* __restrict__ mask,
+                                                                          const double* __restrict__ ratio,
+                                                                          int32_t* __restrict__ status) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t m = int64_t(blockIdx.x) * kWarpsPerCta + warp;
+  if (m >= n) return;
+  const int P = A.P;
+  float* wm = w + m * P;
+  uint8_t* mm = mask + m * P;
+  const double r = ratio[m];
+  if (!(r >= 0.0 && r < 1.0)) {
+    if (lane == 0) status[m] = RINR_ERR_INVALID_INPUT;
+    return;
+  }
+  uint32_t key[KPL];
+#pragma unroll
+  for (int j = 0; j < KPL; ++j) {
+    const int i = 32 * j + lane;
+    key[j] = i < P ? mag_key(wm[i]) : 0xffffffffu;  // padding ranks after every real key
+  }
+  const int64_t k = k_of(r, P);
+  uint32_t dead = 0;  // bit j: entry 32 j + lane is pruned
+  if (k > 0) {
+    uint32_t a = 0, b = 0x7fc00000u;
+    while (a < b) {
+      const uint32_t mid = a + (b - a) / 2;
+      int c = 0;
+#pragma unroll
+      for (int j = 0; j < KPL; ++j) c += key[j] <= mid;
+      if (int64_t(__reduce_add_sync(0xffffffffu, unsigned(c))) >= k) b = mid;
+      else a = mid + 1;
+    }
+    const uint32_t T = a;
+    int lt = 0;
+#pragma unroll
+    for (int j = 0; j < KPL; ++j) lt += key[j] < T;
+    const int64_t need = k - int64_t(__reduce_add_sync(0xffffffffu, unsigned(lt)));
+    const uint32_t below = (1u << lane) - 1u;
+    int64_t base = 0;  // ties in earlier rows
+#pragma unroll
+    for (int j = 0; j < KPL; ++j) {
+      const uint32_t eq = __ballot_sync(0xffffffffu, key[j] == T);
+      const bool d = key[j] < T || (key[j] == T && base + __popc(eq & below) < need);
+      dead |= uint32_t(d) << j;
+      base += __popc(eq);
+    }
+  }
+  // structural check: every matrix keeps an entry (layers are index ranges)
+  uint8_t mk[KPL];
+  uint32_t surv = 0;  // bit l: this lane keeps an entry of matrix l
+  int l = 0;
+#pragma unroll
+  for (int j = 0; j < KPL; ++j) {
+    const int i = 32 * j + lane;
+    mk[j] = i < P ? mm[i] : 0;
+    if (i < P) {
+      while (i >= A.off[l + 1]) ++l;
+      if (mk[j] && !((dead >> j) & 1u)) surv |= 1u << l;
+    }
+  }
+  surv = __reduce_or_sync(0xffffffffu, surv);
+  if (surv != (1u << A.nl) - 1u) {
+    if (lane == 0) status[m] = RINR_ERR_STRUCTURAL;
+    return;
+  }
+#pragma unroll
+  for (int j = 0; j < KPL; ++j) {
+    const int i = 32 * j + lane;
+    if (i < P) {
+      const uint8_t nm = mk[j] && !((dead >> j) & 1u);
+      mm[i] = nm;
+      wm[i] = __fmul_rn(wm[i], nm ? 1.0f : 0.0f);
+    }
+  }
+  if (lane == 0) status[m] = RINR_OK;
+}
+
 __device__ __forceinline__ double warp_min_max(double v, bool is_min) {
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) {
@@ -485,6 +568,18 @@ extern "C" int rinr_prune_l1(const int32_t* dims, int nl, int64_t n, float* d_w,
   if (scope != RINR_PRUNE_GLOBAL && scope != RINR_PRUNE_PER_LAYER)
     return set_error(RINR_ERR_INVALID_INPUT, "unknown prune scope");
   if (n == 0) return RINR_OK;
+  if (scope == RINR_PRUNE_GLOBAL && A.P <= 512 && A.nl <= 31) {  // keys in registers, one warp per model
+    const unsigned grid = unsigned((n + kWarpsPerCta - 1) / kWarpsPerCta);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+#define RINR_PRUNE_REG(K) prune_warp_reg_kernel<K><<<grid, kWarpsPerCta * 32, 0, st>>>(A, n, d_w, d_mask, d_ratio, d_status)
+    if (A.P <= 128) RINR_PRUNE_REG(4);
+    else if (A.P <= 256) RINR_PRUNE_REG(8);
+    else if (A.P <= 320) RINR_PRUNE_REG(10);
+    else if (A.P <= 384) RINR_PRUNE_REG(12);
+    else RINR_PRUNE_REG(16);
+#undef RINR_PRUNE_REG
+    return cuda_check("prune_l1 launch");
+  }
   if (A.P <= kWarpMaxP) {  // small models: one warp each
     const size_t smem = size_t(kWarpsPerCta) * ((A.P * 5 + 15) & ~15);
     if (smem > 48 * 1024 &&

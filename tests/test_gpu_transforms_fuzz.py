@@ -1,7 +1,7 @@
 """Randomised parity sweep of GPU prune_l1 + quantize (csrc/transforms.cu)
 against the oracle (compressor.py:108-218 restated): random architectures on
-both kernel paths (warp per model for P <= 2048, CTA per model above), random
-batch sizes, per-model ratios in [0, 0.99), both scopes, existing masks,
+every kernel path (register-resident keys for global scope with P <= 512,
+warp per model for P <= 2048, CTA per model above), random batch sizes, per-model ratios in [0, 0.99), both scopes, existing masks,
 8 and 16 bits, and adversarial weights (magnitude ties, signed zeros,
 denormals, constant and single-survivor layers).
 
@@ -19,7 +19,8 @@ from transforms_common import cat, split
 pytestmark = pytest.mark.gpu
 
 ARCHS = [(2, 15, 15, 3), (2, 16, 16, 3), (2, 7, 9, 3), (2, 8, 8, 8, 3), (2, 32, 32, 32, 32, 3),
-         (2, 40, 40, 40, 3), (2, 64, 64, 64, 3), (2, 24, 12, 3), (2, 3), (2, 5, 3)]
+         (2, 40, 40, 40, 3), (2, 64, 64, 64, 3), (2, 24, 12, 3), (2, 3), (2, 5, 3), (2, 20, 20, 3),
+         (2, 11, 11, 11, 3)]
 
 
 def _model(rng, dims):
@@ -51,7 +52,7 @@ def _model(rng, dims):
     return w, m, b
 
 
-@pytest.mark.parametrize("seed", range(24))
+@pytest.mark.parametrize("seed", range(32))
 def test_transforms_fuzz(seed):
     from paper_2306_16699_b200 import transforms as T
     from paper_2306_16699_b200.net import Architecture
