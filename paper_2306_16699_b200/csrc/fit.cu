@@ -634,7 +634,9 @@ __device__ __forceinline__ void mma_pass(const FitFrags& F, const uint4* fq, con
   }
 }
 
-// Fold a warp's step sums into its partial row (canonical order; one owner per entry)
+// Write a warp's step sums into its partial row (canonical order).  Every
+// entry of the row has exactly one owner lane, so plain stores suffice (no
+// zeroing, no read-modify-write).
 template <int H>
 __device__ __forceinline__ void fold_grads(const FitGrads& G, float* pw, int lane) {
   using L = FitLayout<H>;
@@ -646,17 +648,17 @@ __device__ __forceinline__ void fold_grads(const FitGrads& G, float* pw, int lan
     for (int j = 0; j < 2; ++j) {
       const int k = 8 * j + cb;
       if (r < H) {
-        if (k < H) pw[2 * H + r * H + k] += G.w1[j][e];
-        else if (k == H) pw[L::P + H + r] += G.w1[j][e];
+        if (k < H) pw[2 * H + r * H + k] = G.w1[j][e];
+        else if (k == H) pw[L::P + H + r] = G.w1[j][e];
       }
     }
     if (cb < 3) {
-      if (r < H) pw[2 * H + H * H + cb * H + r] += G.w2t[e];
-      else if (r == H) pw[L::P + 2 * H + cb] += G.w2t[e];
+      if (r < H) pw[2 * H + H * H + cb * H + r] = G.w2t[e];
+      else if (r == H) pw[L::P + 2 * H + cb] = G.w2t[e];
     }
     if (r < H) {
-      if (cb < 2) pw[2 * r + cb] += G.w0[e];
-      else if (cb == 2) pw[L::P + r] += G.w0[e];
+      if (cb < 2) pw[2 * r + cb] = G.w0[e];
+      else if (cb == 2) pw[L::P + r] = G.w0[e];
     }
   }
 }
@@ -743,7 +745,7 @@ __global__ void __launch_bounds__(kFitThreads / NPX, MMA ? RINR_FIT_MINB : 1) fi
     }
     // this warp's partial gradient row (canonical order), summed over its chunks
     float* pw = part + warp * L::NPAR_PAD;
-    if (!last)
+    if (!last && !MMA)
       for (int i = lane; i < L::NPAR_PAD; i += 32) pw[i] = 0.0f;
     __syncwarp();
     double lp = 0.0;
