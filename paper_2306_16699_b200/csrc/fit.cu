@@ -379,8 +379,9 @@ __device__ __forceinline__ uint4 frag_ld(const uint4* p) {
 }
 
 template <int H>
-// The forward fragments carry omega (z' = omega z straight into the sine):
-// layer 0 and 1 weights / biases are pre-multiplied, the backward ones are not.
+// Every fragment carries omega: forward z' = omega z goes straight into the
+// sine, and the backward products (d W) omega times cos(z') are the reference's
+// (d W) * (omega cos(omega z)).
 __device__ __forceinline__ void load_frags(const float* ws, int lane, float om, FitFrags& F, uint4* fq) {
   using L = FitLayout<H>;
   const int g = lane >> 2, tq = lane & 3;
@@ -394,9 +395,9 @@ __device__ __forceinline__ void load_frags(const float* ws, int lane, float om, 
     uint32_t f[4], b[4];
     pack_act<true>(om * W1(n, 2 * tq), om * W1(n, 2 * tq + 1), f[0], f[2]);
     pack_act<true>(om * W1(n, 2 * tq + 8), om * W1(n, 2 * tq + 9), f[1], f[3]);
-    pack_act<true>(W1(2 * tq, n), W1(2 * tq + 1, n), b[0], b[2]);
-    pack_act<true>(W1(2 * tq + 8, n), W1(2 * tq + 9, n), b[1], b[3]);
-    pack_act<true>(W2(2 * tq, n), W2(2 * tq + 1, n), w2b[2 * j], w2b[2 * j + 1]);
+    pack_act<true>(om * W1(2 * tq, n), om * W1(2 * tq + 1, n), b[0], b[2]);
+    pack_act<true>(om * W1(2 * tq + 8, n), om * W1(2 * tq + 9, n), b[1], b[3]);
+    pack_act<true>(om * W2(2 * tq, n), om * W2(2 * tq + 1, n), w2b[2 * j], w2b[2 * j + 1]);
     fq[32 * j] = make_uint4(f[0], f[1], f[2], f[3]);
     fq[32 * (2 + j)] = make_uint4(b[0], b[1], b[2], b[3]);
 #pragma unroll
@@ -499,8 +500,9 @@ __device__ __forceinline__ void mma_pass(const FitFrags& F, const uint4* fq, con
       for (int e = 0; e < 2; ++e)
         tg[mt][h][e] = ok[mt][h] && 2 * tq + e < 3 ? img[3 * px + 2 * tq + e] : 0.0f;
     }
-  // per-lane unit masks: keep = 1 for real units, one = 1 at the ones column (unit H)
-  float keep[2][2], one[2][2], omk[2][2];  // omk = omega for real units, 0 for pads
+  // per-lane unit masks: keep = 1 for real units, one = 1 at the ones column
+  // (unit H).  Pad units need no mask in the backward: their B columns are 0.
+  float keep[2][2], one[2][2];
 #pragma unroll
   for (int j = 0; j < 2; ++j)
 #pragma unroll
@@ -508,7 +510,6 @@ __device__ __forceinline__ void mma_pass(const FitFrags& F, const uint4* fq, con
       const int u = 8 * j + 2 * tq + e;
       keep[j][e] = u < H ? 1.0f : 0.0f;
       one[j][e] = u == H ? 1.0f : 0.0f;
-      omk[j][e] = u < H ? om : 0.0f;
     }
 #pragma unroll
   for (int mt = 0; mt < MT; ++mt) {
@@ -519,28 +520,30 @@ __device__ __forceinline__ void mma_pass(const FitFrags& F, const uint4* fq, con
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int h = e >> 1;
-        const float z = __fadd_rn(fmaf(y[mt][h], F.w0y[j][e & 1], __fmul_rn(x[mt][h], F.w0x[j][e & 1])), F.b0[j][e & 1]);
-        float sn, cs;
-        __sincosf(z, &sn, &cs);  // z already carries omega
+        const float z = fmaf(x[mt][h], F.w0x[j][e & 1], fmaf(y[mt][h], F.w0y[j][e & 1], F.b0[j][e & 1]));
+        float sn;
+        __sincosf(z, &sn, &c0[j][e]);  // z already carries omega
         v[j][e] = fmaf(sn, keep[j][e & 1], one[j][e & 1]);
-        c0[j][e] = __fmul_rn(omk[j][e & 1], cs);
       }
     uint32_t a0h[4], a0l[4];
     frag_a(v, a0h, a0l);
     // layer 1
     float c1[2][4];
     {
-      float z[2][4] = {};
+      float z[2][4];  // accumulators start at the bias
+#pragma unroll
+      for (int j = 0; j < 2; ++j)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) z[j][e] = F.b1[j][e & 1];
 #pragma unroll
       for (int j = 0; j < 2; ++j) mma3(z[j], a0h, a0l, frag_ld(fq + 32 * j));
 #pragma unroll
       for (int j = 0; j < 2; ++j)
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          float sn, cs;
-          __sincosf(__fadd_rn(z[j][e], F.b1[j][e & 1]), &sn, &cs);
+          float sn;
+          __sincosf(z[j][e], &sn, &c1[j][e]);
           v[j][e] = fmaf(sn, keep[j][e & 1], one[j][e & 1]);
-          c1[j][e] = __fmul_rn(omk[j][e & 1], cs);
         }
     }
     uint32_t a1h[4], a1l[4];
@@ -548,13 +551,13 @@ __device__ __forceinline__ void mma_pass(const FitFrags& F, const uint4* fq, con
     // layer 2, residual, loss, d2 = (2 / size) * resid
     float d2[4];
     {
-      float o[4] = {};
+      float o[4] = {F.b2[0], F.b2[1], F.b2[0], F.b2[1]};
       mma3(o, a1h, a1l, frag_ld(fq + 32 * 4));
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int h = e >> 1;
         const bool val = ok[mt][h] && 2 * tq + (e & 1) < 3;
-        const float r = __fsub_rn(__fadd_rn(o[e], F.b2[e & 1]), tg[mt][h][e & 1]);
+        const float r = __fsub_rn(o[e], tg[mt][h][e & 1]);
         if (val) lp += double(r) * double(r);
         d2[e] = val ? __fmul_rn(s2, r) : 0.0f;
       }
