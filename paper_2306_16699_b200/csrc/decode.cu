@@ -282,8 +282,13 @@ int launch_persist(const StoreView& sv, const int64_t* ids, int64_t n, const Dec
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  // development knob (timing breakdowns only): RINR_DEBUG_SKIP=1 skips phase 2, =2 the dequant, =3 both
+  // development knob for timing breakdowns, compiled only with -DRINR_DEV_KNOBS (it
+  // produces wrong images): RINR_DEBUG_SKIP=1 skips phase 2, =2 the dequant, =3 both
+#ifdef RINR_DEV_KNOBS
   static const int dbg = [] { const char* e = getenv("RINR_DEBUG_SKIP"); return e ? atoi(e) & 3 : 0; }();
+#else
+  constexpr int dbg = 0;
+#endif
   const int overlap = ((flags & RINR_FLAG_OVERLAP_PROLOGUE) ? 1 : 0) | (dbg << 1);
   if (cudaLaunchKernelEx(&cfg, kern, sv, ids, n, a, aug, out, status, omega, lay, overlap) != cudaSuccess)
     return launch_fail("decode_persist launch");
