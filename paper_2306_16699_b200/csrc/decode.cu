@@ -19,8 +19,10 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
+#include <map>
 #include <mutex>
 #include <string>
 #include <unordered_map>
@@ -164,13 +166,16 @@ __global__ void __launch_bounds__(kGenThreads) decode_generic(StoreView sv, cons
 // ============================================================================
 // Launchers
 // ============================================================================
-static int num_sms() {
-  static int sms = [] {
-    int d = 0, v = 148;
-    if (cudaGetDevice(&d) == cudaSuccess) cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d);
-    return v;
-  }();
-  return sms;
+static int num_sms() {  // of the current device, cached per device
+  static std::atomic<int> cache[64];
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= 64) return 148;
+  int v = cache[d].load();
+  if (v == 0) {
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, d) != cudaSuccess || v <= 0) v = 148;
+    cache[d].store(v);
+  }
+  return v;
 }
 
 static int launch_fail(const char* what) {
@@ -178,18 +183,22 @@ static int launch_fail(const char* what) {
   return set_error(RINR_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-// Raise a kernel's dynamic shared-memory limit once (not per launch), so that
-// launches stay legal inside CUDA-graph stream capture.
+// Raise a kernel's dynamic shared-memory limit once per device (not per
+// launch), so that launches stay legal inside CUDA-graph stream capture.  The
+// attribute belongs to the device's context, hence the (device, kernel) key.
 template <class K>
 static bool ensure_smem(K kern, size_t bytes) {
   static std::mutex mu;
-  static std::unordered_map<const void*, size_t> done;
+  static std::map<std::pair<int, const void*>, size_t> done;
   if (bytes <= 48 * 1024) return true;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return false;
+  const auto key = std::make_pair(dev, reinterpret_cast<const void*>(kern));
   std::lock_guard<std::mutex> lock(mu);
-  auto it = done.find(reinterpret_cast<const void*>(kern));
+  auto it = done.find(key);
   if (it != done.end() && it->second >= bytes) return true;
   if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(bytes)) != cudaSuccess) return false;
-  done[reinterpret_cast<const void*>(kern)] = bytes;
+  done[key] = bytes;
   return true;
 }
 

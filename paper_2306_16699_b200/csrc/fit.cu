@@ -20,6 +20,7 @@
 // coordinate tables (MMA pass, ~42 KB).
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
@@ -981,12 +982,16 @@ int launch_fit(const FitArgs& a, cudaStream_t st) {
                                         : sizeof(float) * size_t(a.h + a.wd);
   const size_t smem = smem0 + (MMA ? tabs : 0);
   if (smem > 227 * 1024) return set_error(RINR_ERR_UNSUPPORTED, "fit: image too large for the coordinate tables");
-  static bool attr = false;
-  if (!attr) {
+  // the shared-memory limit is a per-device attribute: raise it once per device
+  static std::atomic<uint64_t> attr_done{0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return set_error(RINR_ERR_CUDA, "fit: no current device");
+  const uint64_t bit = dev < 64 ? uint64_t(1) << dev : 0;
+  if (!(attr_done.load() & bit)) {
     if (cudaFuncSetAttribute(fit_kernel<H, ACC, NPX, MMA>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) !=
         cudaSuccess)
       return set_error(RINR_ERR_CUDA, "fit smem attribute");
-    attr = true;
+    attr_done.fetch_or(bit);
   }
   fit_kernel<H, ACC, NPX, MMA><<<unsigned(a.n), kFitThreads / NPX, smem, st>>>(a);
   const cudaError_t e = cudaGetLastError();
