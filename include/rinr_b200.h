@@ -167,7 +167,10 @@ RINR_API int rinr_dequantize(const rinr_store* store, const int64_t* d_ids, int6
  * d_aug: device float[n*5] per-image parameters (NULL iff aug_mode == NONE).
  * d_status: optional device int32; reset by this call, after the stream
  * reaches it holds 0, or (n - i) for the first id i that is out of range
- * (-> BatchItemError(i, InvalidInputError)).  Stream-ordered, no host sync. */
+ * (-> BatchItemError(i, InvalidInputError)).  Stream-ordered, no host sync.
+ * Both calls launch on the store's device (rinr_store_create's `device`)
+ * whatever the caller's current device is; `stream` and every pointer must
+ * belong to that device. */
 RINR_API int rinr_decode(const rinr_store* store, const int64_t* d_ids, int64_t n,
                 const rinr_decode_params_t* params, const float* d_aug, void* d_out,
                 int32_t* d_status, void* stream);

@@ -537,6 +537,25 @@ int rinr_store_record_meta(const rinr_store* s, int64_t k, int64_t* global_index
   return RINR_OK;
 }
 
+}  // extern "C"
+
+namespace {
+// Launch on the store's device whatever the caller's current device is; a
+// no-op (one cudaGetDevice) when they already match, so it is capture-safe.
+struct StoreDevice {
+  int prev = -1;
+  explicit StoreDevice(int dev) {
+    int cur = 0;
+    if (cudaGetDevice(&cur) == cudaSuccess && cur != dev && cudaSetDevice(dev) == cudaSuccess) prev = cur;
+  }
+  ~StoreDevice() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+}  // namespace
+
+extern "C" {
+
 int rinr_dequantize(const rinr_store* s, const int64_t* d_ids, int64_t n, float* d_out, int64_t out_stride,
                     int32_t* d_status, void* stream) {
   clear_error();
@@ -547,6 +566,7 @@ int rinr_dequantize(const rinr_store* s, const int64_t* d_ids, int64_t n, float*
   if (out_stride < s->max_params)
     return set_error(RINR_ERR_INVALID_INPUT, "out_stride " + std::to_string(out_stride) +
                                                  " < max_param_count " + std::to_string(s->max_params));
+  StoreDevice guard(s->device);
   return rinr_launch_dequantize(s->view, d_ids, n, d_out, out_stride, d_status, stream);
 }
 
@@ -571,6 +591,7 @@ int rinr_decode(const rinr_store* s, const int64_t* d_ids, int64_t n, const rinr
   if (int64_t(p->out_h) * p->out_w > (int64_t(1) << 31) / 4)
     return set_error(RINR_ERR_INVALID_INPUT, "output image too large");
   const HostArch* ua = (s->uniform_arch && !s->archs.empty()) ? &s->archs[0] : nullptr;
+  StoreDevice guard(s->device);
   return rinr_launch_decode(s->view, ua, d_ids, n, p, d_aug, d_out, d_status, stream);
 }
 
