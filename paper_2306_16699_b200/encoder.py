@@ -155,9 +155,10 @@ def train_batch(dm: T.DeviceModels, images: torch.Tensor, lr0: float, steps: int
     sched = torch.from_numpy(_schedule(lr0, steps)).to(images.device)
     p = FitParams(h, w, steps, SIN_MODES[sin], float(lr0), float(dm.arch.omega), cap, sched.data_ptr())
     dims, nl = T._dims(dm.arch)
-    N.check(_lib().rinr_fit(dims, nl, n, dm.w.data_ptr(), dm.b.data_ptr(), dm.mask.data_ptr(), images.data_ptr(),
-                            C.byref(p), curve.data_ptr(), status.data_ptr(), None, None, None,
-                            T._stream(images.device)))
+    with torch.cuda.device(dm.w.device):  # launch on the tensors' device
+        N.check(_lib().rinr_fit(dims, nl, n, dm.w.data_ptr(), dm.b.data_ptr(), dm.mask.data_ptr(), images.data_ptr(),
+                                C.byref(p), curve.data_ptr(), status.data_ptr(), None, None, None,
+                                T._stream(images.device)))
     return curve.cpu().numpy(), status.cpu().numpy()
 
 
@@ -172,9 +173,10 @@ def loss_and_grad_batch(dm: T.DeviceModels, images: torch.Tensor, sin: str = "mu
     status = torch.zeros(n, dtype=torch.int32, device=images.device)
     p = FitParams(h, w, 0, SIN_MODES[sin], 0.0, float(dm.arch.omega), 2, None)
     dims, nl = T._dims(dm.arch)
-    N.check(_lib().rinr_fit(dims, nl, n, dm.w.data_ptr(), dm.b.data_ptr(), dm.mask.data_ptr(), images.data_ptr(),
-                            C.byref(p), curve.data_ptr(), status.data_ptr(), gw.data_ptr(), gb.data_ptr(),
-                            loss.data_ptr(), T._stream(images.device)))
+    with torch.cuda.device(dm.w.device):  # launch on the tensors' device
+        N.check(_lib().rinr_fit(dims, nl, n, dm.w.data_ptr(), dm.b.data_ptr(), dm.mask.data_ptr(), images.data_ptr(),
+                                C.byref(p), curve.data_ptr(), status.data_ptr(), gw.data_ptr(), gb.data_ptr(),
+                                loss.data_ptr(), T._stream(images.device)))
     return loss, gw, gb
 
 
@@ -182,8 +184,9 @@ def render(dm: T.DeviceModels, h: int, w: int, sin: str = "mufu") -> torch.Tenso
     """Clipped [N, h, w, 3] decode of the models (decoder.decode)."""
     out = torch.empty((dm.n, h, w, 3), dtype=torch.float32, device=dm.w.device)
     dims, nl = T._dims(dm.arch)
-    N.check(_lib().rinr_fit_render(dims, nl, dm.n, dm.w.data_ptr(), dm.b.data_ptr(), h, w, float(dm.arch.omega),
-                                   SIN_MODES[sin], out.data_ptr(), T._stream(dm.w.device)))
+    with torch.cuda.device(dm.w.device):  # launch on the tensors' device
+        N.check(_lib().rinr_fit_render(dims, nl, dm.n, dm.w.data_ptr(), dm.b.data_ptr(), h, w, float(dm.arch.omega),
+                                       SIN_MODES[sin], out.data_ptr(), T._stream(dm.w.device)))
     return out
 
 

@@ -112,8 +112,9 @@ def prune_l1(dm: DeviceModels, total_ratio, scope: str = "global", check: bool =
     r = torch.as_tensor(total_ratio, dtype=torch.float64).expand(dm.n).contiguous().to(dm.w.device)
     status = torch.zeros(dm.n, dtype=torch.int32, device=dm.w.device)
     dims, nl = _dims(dm.arch)
-    N.check(N.lib().rinr_prune_l1(dims, nl, dm.n, dm.w.data_ptr(), dm.mask.data_ptr(), r.data_ptr(),
-                                  0 if scope == "global" else 1, status.data_ptr(), _stream(dm.w.device)))
+    with torch.cuda.device(dm.w.device):  # launch on the tensors' device
+        N.check(N.lib().rinr_prune_l1(dims, nl, dm.n, dm.w.data_ptr(), dm.mask.data_ptr(), r.data_ptr(),
+                                      0 if scope == "global" else 1, status.data_ptr(), _stream(dm.w.device)))
     if check:
         _raise_items(status, "prune_l1")
     return status
@@ -151,9 +152,10 @@ def quantize(dm: DeviceModels, mode: str, check: bool = True) -> DeviceQuant:
     codes = torch.zeros_like(dm.w, dtype=torch.int16)  # u16 payload (torch has no uint16 arithmetic)
     status = torch.zeros(dm.n, dtype=torch.int32, device=dev)
     dims, nl = _dims(dm.arch)
-    N.check(N.lib().rinr_quantize(dims, nl, dm.n, bits, dm.w.data_ptr(), dm.mask.data_ptr(), dm.b.data_ptr(),
-                                  scale.data_ptr(), zp.data_ptr(), const.data_ptr(), codes.data_ptr(),
-                                  status.data_ptr(), _stream(dev)))
+    with torch.cuda.device(dm.w.device):  # launch on the tensors' device
+        N.check(N.lib().rinr_quantize(dims, nl, dm.n, bits, dm.w.data_ptr(), dm.mask.data_ptr(), dm.b.data_ptr(),
+                                      scale.data_ptr(), zp.data_ptr(), const.data_ptr(), codes.data_ptr(),
+                                      status.data_ptr(), _stream(dev)))
     if check:
         _raise_items(status, "quantize")
     return DeviceQuant(mode, bits, scale, zp, const.bool(), codes, status)
@@ -178,8 +180,9 @@ def psnr(a: torch.Tensor, b: torch.Tensor, quantized: bool = False):
     count = a[0].numel() if n else 1
     mse = torch.empty(n, dtype=torch.float64, device=a.device)
     out = torch.empty(n, dtype=torch.float64, device=a.device)
-    N.check(N.lib().rinr_psnr(a.data_ptr(), b.data_ptr(), n, count, int(quantized), mse.data_ptr(), out.data_ptr(),
-                              _stream(a.device)))
+    with torch.cuda.device(a.device):  # launch on the tensors' device
+        N.check(N.lib().rinr_psnr(a.data_ptr(), b.data_ptr(), n, count, int(quantized), mse.data_ptr(), out.data_ptr(),
+                                  _stream(a.device)))
     return mse, out
 
 
