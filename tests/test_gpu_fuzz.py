@@ -6,6 +6,8 @@ case builds an archive with the writer, decodes through the C ABI and checks
 the stated bars (fp32 / exact: max-abs <= 1e-3 in [0,1]; bf16: PSNR >= 40 dB;
 dequantised weights bit-exact)."""
 
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -46,7 +48,7 @@ def _random_store(rng):
     return serialize(arc)
 
 
-@pytest.mark.parametrize("seed", range(40))
+@pytest.mark.parametrize("seed", range(int(os.environ.get("RINR_FUZZ_SEEDS", 40))))
 def test_decode_fuzz(seed):
     from paper_2306_16699_b200 import Store
     rng = np.random.default_rng(1000 + seed)
