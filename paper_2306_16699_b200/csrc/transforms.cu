@@ -394,25 +394,33 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) prune_warp_reg_kernel(TArch
     const int i = 32 * j + lane;
     key[j] = i < P ? mag_key(wm[i]) : 0xffffffffu;  // padding ranks after every real key
   }
-  const int64_t k = k_of(r, P);
+  const int k = int(k_of(r, P));  // P <= 512
   uint32_t dead = 0;  // bit j: entry 32 j + lane is pruned
   if (k > 0) {
-    uint32_t a = 0, b = 0x7fc00000u;
+    // T lies between the smallest and the largest real key
+    uint32_t lo = 0xffffffffu, hi = 0u;
+#pragma unroll
+    for (int j = 0; j < KPL; ++j)
+      if (32 * j + lane < P) {
+        lo = min(lo, key[j]);
+        hi = max(hi, key[j]);
+      }
+    uint32_t a = __reduce_min_sync(0xffffffffu, lo), b = __reduce_max_sync(0xffffffffu, hi);
     while (a < b) {
       const uint32_t mid = a + (b - a) / 2;
       int c = 0;
 #pragma unroll
       for (int j = 0; j < KPL; ++j) c += key[j] <= mid;
-      if (int64_t(__reduce_add_sync(0xffffffffu, unsigned(c))) >= k) b = mid;
+      if (int(__reduce_add_sync(0xffffffffu, unsigned(c))) >= k) b = mid;
       else a = mid + 1;
     }
     const uint32_t T = a;
     int lt = 0;
 #pragma unroll
     for (int j = 0; j < KPL; ++j) lt += key[j] < T;
-    const int64_t need = k - int64_t(__reduce_add_sync(0xffffffffu, unsigned(lt)));
+    const int need = k - int(__reduce_add_sync(0xffffffffu, unsigned(lt)));
     const uint32_t below = (1u << lane) - 1u;
-    int64_t base = 0;  // ties in earlier rows
+    int base = 0;  // ties in earlier rows
 #pragma unroll
     for (int j = 0; j < KPL; ++j) {
       const uint32_t eq = __ballot_sync(0xffffffffu, key[j] == T);
