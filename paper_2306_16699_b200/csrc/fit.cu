@@ -501,6 +501,7 @@ __device__ __forceinline__ void mma_pass(const FitFrags& F, const uint4* fq, con
       for (int e = 0; e < 2; ++e)
         tg[mt][h][e] = ok[mt][h] && 2 * tq + e < 3 ? img[3 * px + 2 * tq + e] : 0.0f;
     }
+  float lpf = 0.0f;  // this pass's squared residuals (f32 partial, added to the f64 total below)
   // per-lane unit masks: keep = 1 for real units, one = 1 at the ones column
   // (unit H).  Pad units need no mask in the backward: their B columns are 0.
   float keep[2][2], one[2][2];
@@ -559,7 +560,7 @@ __device__ __forceinline__ void mma_pass(const FitFrags& F, const uint4* fq, con
         const int h = e >> 1;
         const bool val = ok[mt][h] && 2 * tq + (e & 1) < 3;
         const float r = __fsub_rn(o[e], tg[mt][h][e & 1]);
-        if (val) lp += double(r) * double(r);
+        if (val) lpf = fmaf(r, r, lpf);
         d2[e] = val ? __fmul_rn(s2, r) : 0.0f;
       }
     }
@@ -636,6 +637,7 @@ __device__ __forceinline__ void mma_pass(const FitFrags& F, const uint4* fq, con
       mma16816(G.w0, th, b0l, b1l);
     }
   }
+  lp += double(lpf);
 }
 
 // Write a warp's step sums into its partial row (canonical order).  Every
