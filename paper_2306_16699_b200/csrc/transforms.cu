@@ -377,6 +377,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) prune_warp_reg_kernel(TArch
                                                                           uint8_t* __restrict__ mask,
                                                                           const double* __restrict__ ratio,
                                                                           int32_t* __restrict__ status) {
+  __shared__ uint32_t sel_cand[kWarpsPerCta][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t m = int64_t(blockIdx.x) * kWarpsPerCta + warp;
   if (m >= n) return;
@@ -406,13 +407,43 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) prune_warp_reg_kernel(TArch
         hi = max(hi, key[j]);
       }
     uint32_t a = __reduce_min_sync(0xffffffffu, lo), b = __reduce_max_sync(0xffffffffu, hi);
-    while (a < b) {
+    // invariant: ca = count(key < a) < k <= cb = count(key <= b); bisect
+    // until at most 32 keys lie in [a, b], then select among those directly
+    int ca = 0, cb = P;
+    while (a < b && cb - ca > 32) {
       const uint32_t mid = a + (b - a) / 2;
       int c = 0;
 #pragma unroll
       for (int j = 0; j < KPL; ++j) c += key[j] <= mid;
-      if (int(__reduce_add_sync(0xffffffffu, unsigned(c))) >= k) b = mid;
-      else a = mid + 1;
+      c = int(__reduce_add_sync(0xffffffffu, unsigned(c)));
+      if (c >= k) {
+        b = mid;
+        cb = c;
+      } else {
+        a = mid + 1;
+        ca = c;
+      }
+    }
+    if (a < b) {
+      // compact the <= 32 keys of [a, b] (padding keys are above b) into one
+      // slot per lane, then T = the smallest candidate with
+      // count(candidates <= T) >= k - ca
+      uint32_t* cand = sel_cand[warp];
+      const uint32_t below = (1u << lane) - 1u, span = b - a;
+      int base = 0;
+#pragma unroll
+      for (int j = 0; j < KPL; ++j) {
+        const bool in = key[j] - a <= span;
+        const uint32_t bal = __ballot_sync(0xffffffffu, in);
+        if (in) cand[base + __popc(bal & below)] = key[j];
+        base += __popc(bal);
+      }
+      __syncwarp();
+      const uint32_t mine = lane < base ? cand[lane] : 0xffffffffu;
+      int le = 0;
+      for (int q = 0; q < base; ++q) le += cand[q] <= mine;
+      a = __reduce_min_sync(0xffffffffu, lane < base && le >= k - ca ? mine : 0xffffffffu);
+      __syncwarp();
     }
     const uint32_t T = a;
     int lt = 0;
