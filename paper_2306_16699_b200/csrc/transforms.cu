@@ -50,11 +50,42 @@ __device__ __forceinline__ int block_sum(int v, int* red) {
   return t;
 }
 
+// Block-wide min of one u32 per thread (all threads must call).
+__device__ __forceinline__ uint32_t block_min_u32(uint32_t v, int* red) {
+  v = __reduce_min_sync(0xffffffffu, v);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) red[warp] = int(v);
+  __syncthreads();
+  uint32_t t = uint32_t(red[0]);
+  for (int i = 1; i < (kThreads >> 5); ++i) t = min(t, uint32_t(red[i]));
+  return t;
+}
+
+// Block-wide exclusive prefix sum over threads in index order.
+__device__ __forceinline__ int block_excl_scan(int v, int* red) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  int inc = v;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const int o = __shfl_up_sync(0xffffffffu, inc, d);
+    if (lane >= d) inc += o;
+  }
+  __syncthreads();
+  if (lane == 31) red[warp] = inc;
+  __syncthreads();
+  int before = 0;
+  for (int i = 0; i < warp; ++i) before += red[i];
+  return before + inc - v;
+}
+
 // Doom the k smallest keys of [lo, hi) (ties by position) in `dead`:
 // T = the smallest key with count(key <= T) >= k, found by bisection over
-// the 31-bit key space; keys < T are doomed, and of the keys == T the first
+// the range's key span (finished by a direct select once <= kThreads keys
+// remain in the bracket); keys < T are doomed, and of the keys == T the first
 // k - count(key < T) in index order.
-__device__ void select_smallest(const uint32_t* key, uint8_t* dead, int lo, int hi, int64_t k, int* red) {
+__device__ void select_smallest(const uint32_t* key, uint8_t* dead, int lo, int hi, int64_t k, int* red,
+                                uint32_t* cand) {
   const int tid = threadIdx.x;
   const int len = hi - lo;
   const int per = (len + kThreads - 1) / kThreads;
@@ -64,13 +95,42 @@ __device__ void select_smallest(const uint32_t* key, uint8_t* dead, int lo, int 
     __syncthreads();
     return;
   }
-  uint32_t a = 0, b = 0x7fc00000u;
-  while (a < b) {
+  // T lies between the smallest and the largest key of the range
+  uint32_t kmin = 0xffffffffu, kmax = 0u;
+  for (int i = c0; i < c1; ++i) {
+    kmin = min(kmin, key[i]);
+    kmax = max(kmax, key[i]);
+  }
+  uint32_t a = block_min_u32(kmin, red), b = ~block_min_u32(~kmax, red);
+  // invariant: ca = count(key < a) < k <= cb = count(key <= b); bisect until
+  // at most one key per thread lies in [a, b], then select among those
+  int64_t ca = 0, cb = len;
+  while (a < b && cb - ca > kThreads) {
     const uint32_t mid = a + (b - a) / 2;
     int c = 0;
     for (int i = c0; i < c1; ++i) c += key[i] <= mid;
-    if (block_sum(c, red) >= k) b = mid;
-    else a = mid + 1;
+    const int64_t cm = block_sum(c, red);
+    if (cm >= k) {
+      b = mid;
+      cb = cm;
+    } else {
+      a = mid + 1;
+      ca = cm;
+    }
+  }
+  if (a < b) {
+    const uint32_t span = b - a;
+    int mine = 0;
+    for (int i = c0; i < c1; ++i) mine += key[i] - a <= span;
+    int pos = block_excl_scan(mine, red);
+    for (int i = c0; i < c1; ++i)
+      if (key[i] - a <= span) cand[pos++] = key[i];
+    __syncthreads();
+    const int total = int(cb - ca);
+    const uint32_t v = tid < total ? cand[tid] : 0xffffffffu;
+    int le = 0;
+    for (int q = 0; q < total; ++q) le += cand[q] <= v;
+    a = block_min_u32(tid < total && le >= k - ca ? v : 0xffffffffu, red);
   }
   const uint32_t T = a;
   int lt = 0, eq = 0;
@@ -115,6 +175,7 @@ __global__ void __launch_bounds__(kThreads) prune_kernel(TArch A, float* __restr
                                                          int32_t* __restrict__ status) {
   extern __shared__ __align__(16) uint8_t sm[];
   __shared__ int red[32 + kThreads];
+  __shared__ uint32_t cand[kThreads];
   const int64_t m = blockIdx.x;
   const int P = A.P;
   uint32_t* key = reinterpret_cast<uint32_t*>(sm);
@@ -129,10 +190,10 @@ __global__ void __launch_bounds__(kThreads) prune_kernel(TArch A, float* __restr
   for (int i = threadIdx.x; i < P; i += kThreads) key[i] = mag_key(wm[i]);
   __syncthreads();
   if (scope == RINR_PRUNE_GLOBAL) {
-    select_smallest(key, dead, 0, P, k_of(r, P), red);
+    select_smallest(key, dead, 0, P, k_of(r, P), red, cand);
   } else {
     for (int l = 0; l < A.nl; ++l)
-      select_smallest(key, dead, A.off[l], A.off[l + 1], k_of(r, A.off[l + 1] - A.off[l]), red);
+      select_smallest(key, dead, A.off[l], A.off[l + 1], k_of(r, A.off[l + 1] - A.off[l]), red, cand);
   }
   // new mask = old & ~doomed; no matrix may lose every entry (compressor.py:133-137)
   bool ok = true;
@@ -281,7 +342,8 @@ constexpr int kWarpMaxP = 2048;
 constexpr int kWarpsPerCta = 8;
 
 // Warp-level select_smallest over [lo, hi) of this warp's keys (same rule).
-__device__ void warp_select(const uint32_t* key, uint8_t* dead, int lo, int hi, int64_t k, int lane) {
+__device__ void warp_select(const uint32_t* key, uint8_t* dead, int lo, int hi, int64_t k, int lane,
+                            uint32_t* cand) {
   const int len = hi - lo;
   const int per = (len + 31) / 32;
   const int c0 = lo + lane * per, c1 = min(hi, c0 + per);
@@ -290,13 +352,49 @@ __device__ void warp_select(const uint32_t* key, uint8_t* dead, int lo, int hi, 
     __syncwarp();
     return;
   }
-  uint32_t a = 0, b = 0x7fc00000u;
-  while (a < b) {
+  uint32_t kmin = 0xffffffffu, kmax = 0u;
+  for (int i = c0; i < c1; ++i) {
+    kmin = min(kmin, key[i]);
+    kmax = max(kmax, key[i]);
+  }
+  uint32_t a = __reduce_min_sync(0xffffffffu, kmin), b = __reduce_max_sync(0xffffffffu, kmax);
+  // invariant: ca = count(key < a) < k <= cb = count(key <= b); bisect until
+  // at most 32 keys lie in [a, b], then select among those (as in
+  // prune_warp_reg_kernel)
+  int ca = 0, cb = len;
+  while (a < b && cb - ca > 32) {
     const uint32_t mid = a + (b - a) / 2;
     int c = 0;
     for (int i = c0; i < c1; ++i) c += key[i] <= mid;
-    if (int64_t(__reduce_add_sync(0xffffffffu, unsigned(c))) >= k) b = mid;
-    else a = mid + 1;
+    c = int(__reduce_add_sync(0xffffffffu, unsigned(c)));
+    if (c >= k) {
+      b = mid;
+      cb = c;
+    } else {
+      a = mid + 1;
+      ca = c;
+    }
+  }
+  if (a < b) {
+    const uint32_t span = b - a;
+    int mine = 0;
+    for (int i = c0; i < c1; ++i) mine += key[i] - a <= span;
+    int incl = mine;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const int t = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= d) incl += t;
+    }
+    int pos = incl - mine;
+    for (int i = c0; i < c1; ++i)
+      if (key[i] - a <= span) cand[pos++] = key[i];
+    __syncwarp();
+    const int total = cb - ca;
+    const uint32_t v = lane < total ? cand[lane] : 0xffffffffu;
+    int le = 0;
+    for (int q = 0; q < total; ++q) le += cand[q] <= v;
+    a = __reduce_min_sync(0xffffffffu, lane < total && le >= k - ca ? v : 0xffffffffu);
+    __syncwarp();
   }
   const uint32_t T = a;
   int lt = 0, eq = 0;
@@ -329,6 +427,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) prune_warp_kernel(TArch A, 
                                                                       const double* __restrict__ ratio, int scope,
                                                                       int32_t* __restrict__ status) {
   extern __shared__ __align__(16) uint8_t sm[];
+  __shared__ uint32_t sel_cand[kWarpsPerCta][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t m = int64_t(blockIdx.x) * kWarpsPerCta + warp;
   if (m >= n) return;
@@ -346,9 +445,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) prune_warp_kernel(TArch A, 
   for (int i = lane; i < P; i += 32) key[i] = mag_key(wm[i]);
   __syncwarp();
   if (scope == RINR_PRUNE_GLOBAL) {
-    warp_select(key, dead, 0, P, k_of(r, P), lane);
+    warp_select(key, dead, 0, P, k_of(r, P), lane, sel_cand[warp]);
   } else {
-    for (int l = 0; l < A.nl; ++l) warp_select(key, dead, A.off[l], A.off[l + 1], k_of(r, A.off[l + 1] - A.off[l]), lane);
+    for (int l = 0; l < A.nl; ++l) warp_select(key, dead, A.off[l], A.off[l + 1], k_of(r, A.off[l + 1] - A.off[l]), lane,
+                                              sel_cand[warp]);
   }
   bool ok = true;
   for (int l = 0; l < A.nl; ++l) {
