@@ -472,11 +472,15 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) prune_warp_kernel(TArch A, 
 // in registers, interleaved (key j of a lane is entry 32 j + lane, so global
 // loads and stores are coalesced): the same bisection for T, with per-lane
 // counts and one REDUX per step, then ties ranked in index order by ballots.
+// CTAs per SM: the most that fit each key count without spills (old mask
+// and doomed bits are packed into one word per lane).
 template <int KPL>
-__global__ void __launch_bounds__(kWarpsPerCta * 32) prune_warp_reg_kernel(TArch A, int64_t n, float* __restrict__ w,
-                                                                          uint8_t* __restrict__ mask,
-                                                                          const double* __restrict__ ratio,
-                                                                          int32_t* __restrict__ status) {
+constexpr int prune_reg_ctas() { return KPL >= 16 ? 4 : (KPL >= 10 ? 5 : 6); }
+
+template <int KPL>
+__global__ void __launch_bounds__(kWarpsPerCta * 32, prune_reg_ctas<KPL>())
+    prune_warp_reg_kernel(TArch A, int64_t n, float* __restrict__ w, uint8_t* __restrict__ mask,
+                          const double* __restrict__ ratio, int32_t* __restrict__ status) {
   __shared__ uint32_t sel_cand[kWarpsPerCta][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int64_t m = int64_t(blockIdx.x) * kWarpsPerCta + warp;
@@ -561,16 +565,17 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) prune_warp_reg_kernel(TArch
     }
   }
   // structural check: every matrix keeps an entry (layers are index ranges)
-  uint8_t mk[KPL];
+  uint32_t keep = 0;  // bit j: entry 32 j + lane stays (old mask and not doomed)
   uint32_t surv = 0;  // bit l: this lane keeps an entry of matrix l
   int l = 0;
 #pragma unroll
   for (int j = 0; j < KPL; ++j) {
     const int i = 32 * j + lane;
-    mk[j] = i < P ? mm[i] : 0;
     if (i < P) {
+      const bool kp = mm[i] && !((dead >> j) & 1u);
+      keep |= uint32_t(kp) << j;
       while (i >= A.off[l + 1]) ++l;
-      if (mk[j] && !((dead >> j) & 1u)) surv |= 1u << l;
+      if (kp) surv |= 1u << l;
     }
   }
   surv = __reduce_or_sync(0xffffffffu, surv);
@@ -582,7 +587,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) prune_warp_reg_kernel(TArch
   for (int j = 0; j < KPL; ++j) {
     const int i = 32 * j + lane;
     if (i < P) {
-      const uint8_t nm = mk[j] && !((dead >> j) & 1u);
+      const uint8_t nm = (keep >> j) & 1u;
       mm[i] = nm;
       wm[i] = __fmul_rn(wm[i], nm ? 1.0f : 0.0f);
     }
