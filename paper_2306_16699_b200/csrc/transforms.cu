@@ -230,6 +230,16 @@ __device__ __forceinline__ double block_min_max(double v, bool is_min, double* d
 }
 
 // grid: n x (nl - 2), one CTA per (model, hidden matrix)
+// a / b correctly rounded for b > 0 from y = RN(1/b): q = RN(a y) is within
+// one ulp, r = a - b q is exact (FMA), and RN(q + r y) is the correctly rounded
+// quotient (Markstein's theorem); quotients here stay in the normal range
+// (|a| is a float, b >= 2^-149 / 65535). Zero keeps its sign as in a / b.
+__device__ __forceinline__ double div_by_rcp(double a, double b, double y) {
+  if (a == 0.0) return a;
+  const double q = __dmul_rn(a, y);
+  return __fma_rn(__fma_rn(-q, b, a), y, q);
+}
+
 __global__ void __launch_bounds__(kThreads) quantize_kernel(TArch A, int bits, float* __restrict__ w,
                                                             const uint8_t* __restrict__ mask,
                                                             const float* __restrict__ bias, double* __restrict__ d_scale,
@@ -287,16 +297,16 @@ __global__ void __launch_bounds__(kThreads) quantize_kernel(TArch A, int bits, f
     for (int i = lo + threadIdx.x; i < hi; i += kThreads) cm[i] = 0;
     return;
   }
-  const double zpd = double(zp);
+  const double zpd = double(zp), rs = __drcp_rn(scale);
   for (int i = lo + threadIdx.x; i < hi; i += kThreads) {
     // codes = clip(round(w / scale) + zp, 0, qmax); w = f32(scale * (codes - zp)) * mask
-    double c = __dadd_rn(rint(__ddiv_rn(double(wm[i]), scale)), zpd);
+    double c = __dadd_rn(rint(div_by_rcp(double(wm[i]), scale, rs)), zpd);
     c = fmin(fmax(c, 0.0), qmax);
     const float q = __double2float_rn(__dmul_rn(scale, __dsub_rn(c, zpd)));
     const float wn = __fmul_rn(q, mm[i] ? 1.0f : 0.0f);
     wm[i] = wn;
     // quantize_codes recomputes from the snapped weights (compressor.py:215-217)
-    double c2 = __dadd_rn(rint(__ddiv_rn(double(wn), scale)), zpd);
+    double c2 = __dadd_rn(rint(div_by_rcp(double(wn), scale, rs)), zpd);
     c2 = fmin(fmax(c2, 0.0), qmax);
     cm[i] = uint16_t(c2);
   }
@@ -656,14 +666,14 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32) quantize_warp_kernel(
       for (int i = lo + lane; i < hi; i += 32) cm[i] = 0;
       continue;
     }
-    const double zpd = double(zp);
+    const double zpd = double(zp), rs = __drcp_rn(scale);
     for (int i = lo + lane; i < hi; i += 32) {
-      double c = __dadd_rn(rint(__ddiv_rn(double(wm[i]), scale)), zpd);
+      double c = __dadd_rn(rint(div_by_rcp(double(wm[i]), scale, rs)), zpd);
       c = fmin(fmax(c, 0.0), qmax);
       const float q = __double2float_rn(__dmul_rn(scale, __dsub_rn(c, zpd)));
       const float wn = __fmul_rn(q, mm[i] ? 1.0f : 0.0f);
       wm[i] = wn;
-      double c2 = __dadd_rn(rint(__ddiv_rn(double(wn), scale)), zpd);
+      double c2 = __dadd_rn(rint(div_by_rcp(double(wn), scale, rs)), zpd);
       c2 = fmin(fmax(c2, 0.0), qmax);
       cm[i] = uint16_t(c2);
     }
