@@ -100,3 +100,44 @@ def test_transforms_fuzz(seed):
             assert q.scale[k, i - 1].item() == scale and q.zero_point[k, i - 1].item() == zp, (seed, k, i)
             if not const:
                 np.testing.assert_array_equal(split(codes[k], dims)[i], O.quantize_codes(qw[i], scale, zp, bits))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("bits,arch", [(8, (2, 15, 15, 3)), (16, (2, 15, 15, 3)), (8, (2, 40, 40, 40, 40, 40, 40, 40, 40, 40, 3))])
+def test_quantize_half_step_weights(bits, arch):
+    """Weights on and one float ulp either side of mn + (k + 1/2) scale: the
+    f64 quotient w / scale lands next to a rounding boundary, so the GPU's
+    reciprocal + FMA quotient must round exactly like the oracle's true
+    division (compressor.py:180-202 via O.quantize)."""
+    from paper_2306_16699_b200 import transforms as T
+    from paper_2306_16699_b200.net import Architecture
+    rng = np.random.default_rng(77 + bits)
+    qmax = (1 << bits) - 1
+    models = []
+    for _ in range(24):
+        w, m, b = _model(rng, arch)
+        m = [np.ones_like(x, dtype=bool) for x in m]
+        for i in range(1, len(arch) - 2):
+            lo, hi = np.float32(rng.uniform(-2, -0.01)), np.float32(rng.uniform(0.01, 2))
+            scale = (float(hi) - float(lo)) / qmax
+            k = rng.integers(0, qmax, w[i].size)
+            v = (float(lo) + (k + 0.5) * scale).astype(np.float32)
+            v = np.where(rng.random(v.size) < 1 / 3, np.nextafter(v, np.float32(-9)),
+                         np.where(rng.random(v.size) < 0.5, np.nextafter(v, np.float32(9)), v))
+            v[0], v[1] = lo, hi
+            w[i] = v.reshape(w[i].shape).astype(np.float32)
+        models.append((w, m, b))
+    dm = T.DeviceModels(Architecture(arch),
+                        torch.from_numpy(np.stack([cat(w) for w, _, _ in models]).astype(np.float32)).cuda(),
+                        torch.from_numpy(np.stack([cat(m) for _, m, _ in models]).astype(np.uint8)).cuda(),
+                        torch.from_numpy(np.stack([cat(b) for _, _, b in models]).astype(np.float32)).cuda())
+    q = T.quantize(dm, "affine8" if bits == 8 else "affine16", check=False)
+    assert not q.status.any()
+    w_q = dm.w.cpu().numpy()
+    codes = q.codes.cpu().numpy().view(np.uint16)
+    for k, (w, m, b) in enumerate(models):
+        qw, info = O.quantize(w, m, b, bits)
+        np.testing.assert_array_equal(w_q[k].view(np.uint32), cat(qw).view(np.uint32), err_msg=f"model {k}")
+        for i, (scale, zp, const) in info.items():
+            if not const:
+                np.testing.assert_array_equal(split(codes[k], arch)[i], O.quantize_codes(qw[i], scale, zp, bits))
