@@ -11,6 +11,7 @@ from __future__ import annotations
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 from pathlib import Path
 
 PKG = Path(__file__).resolve().parent
@@ -38,8 +39,7 @@ def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and not _stale():
         return LIB
     LIB_DIR.mkdir(exist_ok=True)
-    objs = []
-    for src in SOURCES:
+    def compile_one(src: Path) -> str:
         obj = LIB_DIR / (src.stem + ".o")
         cmd = [NVCC, *ARCH, *FLAGS, "-I", str(ROOT / "include"), "-c", str(src), "-o", str(obj)]
         if src.suffix == ".cpp":
@@ -52,7 +52,11 @@ def build(force: bool = False, verbose: bool = False) -> Path:
             raise RuntimeError(f"nvcc failed on {src.name}")
         if verbose:
             sys.stderr.write(res.stderr)
-        objs.append(str(obj))
+        return str(obj)
+
+    # translation units compile independently: one nvcc per source, in parallel
+    with ThreadPoolExecutor(max_workers=len(SOURCES)) as pool:
+        objs = list(pool.map(compile_one, SOURCES))
     tmp = LIB.with_suffix(".so.tmp")
     cmd = [NVCC, *ARCH, "-shared", "-o", str(tmp), *objs, "-Xcompiler", "-fPIC"]
     res = subprocess.run(cmd, capture_output=True, text=True)

@@ -114,26 +114,39 @@ def hidden_layer_indices(n_layers: int) -> range:
     return range(1, n_layers - 1)
 
 
-def prune_l1_batch(mb: ModelBatch, ratios) -> ModelBatch:
-    """Global L1 prune of every record to its own total zero ratio."""
+def prune_l1_batch(mb: ModelBatch, ratios, scope: str = "global") -> ModelBatch:
+    """L1 prune of every record to its own total zero ratio: ``scope``
+    "global" ranks |w| over all matrices jointly, "per_layer" within each
+    matrix (compressor.py:108-152)."""
     ratios = np.broadcast_to(np.asarray(ratios, np.float64), (mb.n,))
     if np.any(~((ratios >= 0.0) & (ratios < 1.0))):
         raise InvalidInputError("total_ratio must be in [0, 1)")
+    if scope not in ("global", "per_layer"):
+        raise InvalidInputError(f"unknown scope {scope!r}")
+
+    def doomed_of(ws):
+        mags = np.concatenate([np.abs(w.reshape(mb.n, -1)).astype(np.float64) for w in ws], axis=1)
+        total = mags.shape[1]
+        order = np.argsort(mags, axis=1, kind="stable")
+        rank = np.empty_like(order)
+        np.put_along_axis(rank, order, np.arange(total)[None, :].repeat(mb.n, 0), axis=1)
+        k = np.floor(ratios * total + 0.5).astype(np.int64)
+        return rank < k[:, None]
+
     sizes = [w.shape[1] * w.shape[2] for w in mb.w]
-    mags = np.concatenate([np.abs(w.reshape(mb.n, -1)).astype(np.float64) for w in mb.w], axis=1)
-    total = mags.shape[1]
-    order = np.argsort(mags, axis=1, kind="stable")
-    rank = np.empty_like(order)
-    np.put_along_axis(rank, order, np.arange(total)[None, :].repeat(mb.n, 0), axis=1)
-    k = np.floor(ratios * total + 0.5).astype(np.int64)
-    doomed = rank < k[:, None]
+    if scope == "global":
+        doomed = doomed_of(mb.w)
+    else:
+        doomed = np.concatenate([doomed_of([w]) for w in mb.w], axis=1)
     out_w, out_m = [], []
     off = 0
     for w, m, sz in zip(mb.w, mb.mask, sizes):
         keep = ~doomed[:, off:off + sz].reshape(m.shape) & m
         off += sz
         if not keep.reshape(mb.n, -1).any(axis=1).all():
-            raise StructuralError(f"ratio would zero an entire layer ({m.shape[1]}x{m.shape[2]})")
+            bad = float(ratios[int(np.argmin(keep.reshape(mb.n, -1).any(axis=1)))])
+            raise StructuralError(f"ratio {bad} would zero an entire layer" +
+                                  (f" ({m.shape[1]}x{m.shape[2]})" if scope == "global" else ""))
         out_m.append(keep)
         out_w.append(np.multiply(w, keep))  # w * False -> -0.0 for negative w, as the reference
     return ModelBatch(mb.arch, out_w, [b.copy() for b in mb.b], out_m, mb.source_h, mb.source_w,
@@ -191,10 +204,9 @@ def quantize_codes_batch(mb: ModelBatch, layer: int) -> np.ndarray:
 # ---- single-model API with the reference's signatures -----------------------
 
 def prune_l1(model, total_ratio: float, scope: str = "global") -> InrModel:
-    if scope != "global":
-        raise InvalidInputError(f"unknown scope {scope!r}" if scope != "per_layer"
-                                else "per_layer pruning is not part of the decode path")
-    return prune_l1_batch(ModelBatch.from_models([model]), total_ratio).model(0)
+    if not (0.0 <= total_ratio < 1.0):
+        raise InvalidInputError(f"total_ratio must be in [0, 1), got {total_ratio}")
+    return prune_l1_batch(ModelBatch.from_models([model]), total_ratio, scope).model(0)
 
 
 def quantize(model, mode: str) -> InrModel:

@@ -222,6 +222,16 @@ __device__ __forceinline__ float value_at(const uint8_t* rec, const ValueRecipe&
   }
 }
 
+// An affine8 hidden layer may feed the MMA as integer B = code - zero_point
+// (exact in bf16) only when every such difference is an integer of magnitude
+// <= 256: codes are 0..255, so zero_point must lie in [-1, 256].  The
+// reference quantizer gives zero points outside that range when all kept
+// weights share one sign (compressor.py:175-185); those layers take the
+// float hi/lo path instead.
+__device__ __forceinline__ bool int_b_exact(const DLayer& L) {
+  return L.tag == TAG_A8 && !L.cst && L.zp >= -1 && L.zp <= 256;
+}
+
 __device__ __forceinline__ float dq_bias(const uint8_t* rec, const DLayer& L, int o) {
   return __uint_as_float(ld_u32u(rec, L.bias_off + 4u * o));
 }

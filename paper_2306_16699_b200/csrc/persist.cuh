@@ -520,7 +520,7 @@ __global__ void __launch_bounds__(NW * 32, (NW < 16 ? 16 / NW : 1))
           const DLayer L = parse_layer(rec, lo[l], lo[l + 1], HID, HID);
           const WarpBits B = warp_bits(rec, L, lane);
           const ValueRecipe R = value_recipe(L);
-          const bool int_b = M::INTB || (L.tag == TAG_A8 && !L.cst);
+          const bool int_b = M::INTB || int_b_exact(L);
           uint4* fr = reinterpret_cast<uint4*>(net.fragH + (l - 1) * C::KT * C::NT * 32 * 4);
           if (int_b) {
 #pragma unroll
@@ -567,7 +567,7 @@ __global__ void __launch_bounds__(NW * 32, (NW < 16 ? 16 / NW : 1))
         __syncwarp();
       }
       const bool hidden = l > 0 && l < NL - 1;
-      const bool int_b = hidden && L.tag == TAG_A8 && !L.cst;
+      const bool int_b = hidden && int_b_exact(L);
       Net net(nets + i * lay.net_words);
       if (l == 0) {
         for (int j = lane; j < L.n; j += 32)

@@ -135,8 +135,11 @@ static void parse_body(const uint8_t* b, size_t len, const std::string& ctx, Par
       throw ParseError{RINR_ERR_INTEGRITY, ctx + ": layer " + std::to_string(l) + " has bad tag/form " +
                                                std::to_string(tag) + "/" + std::to_string(form)};
     bool affine = tag == TAG_A8 || tag == TAG_A16;
-    if (l > 0 && l + 2 < nd && !(tag == TAG_A8 && !cst)) out.hidden_int8 = false;
-    if (affine) take(12);
+    int32_t zp = 0;
+    if (affine) zp = rd<int32_t>(take(12) + 8);
+    // integer-B MMA operand only when every code - zp is exact in bf16
+    // (device_common.cuh int_b_exact)
+    if (l > 0 && l + 2 < nd && !(tag == TAG_A8 && !cst && zp >= -1 && zp <= 256)) out.hidden_int8 = false;
     size_t kept = n;
     if (form != FORM_DENSE) {
       const uint8_t* bits = take((n + 7) / 8);

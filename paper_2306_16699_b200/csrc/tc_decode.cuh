@@ -349,7 +349,7 @@ __global__ void __launch_bounds__(4 * T * 32, 1)
         const DLayer L = parse_layer(rec, lo[l], lo[l + 1], fi, fo);
         const uint32_t* words = pfx + i * lay.pfx_words + l * 2 * KW;
         const bool hidden = l > 0 && l < NL - 1;
-        const bool int_b = hidden && L.tag == TAG_A8 && !L.cst;
+        const bool int_b = hidden && int_b_exact(L);
         Net net(nets + size_t(i) * lay.net_bytes);
         if (is_bias) {
           const float bb = dq_bias(rec, L, o);

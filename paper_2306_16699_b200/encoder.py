@@ -33,7 +33,7 @@ import torch
 from . import _native as N
 from . import transforms as T
 from .compressor import ModelBatch, dynamic_ratio, get_schedule
-from .errors import BatchItemError, InvalidInputError, TrainingError
+from .errors import ERR_STRUCTURAL, BatchItemError, InvalidInputError, StructuralError, TrainingError
 from .image import ImageBuffer
 from .net import Architecture, init
 
@@ -213,6 +213,22 @@ def _train_round(dm, images, lr0, steps, cfg, reports, alive, on_error):
         reports[i].loss_curve.extend(float(v) for v in curves[i] if not math.isnan(v))
 
 
+def _prune_round(dm, ratios, alive, on_error):
+    """Per-image prune (GPU prune_l1, check=False): an image whose prune would
+    empty a layer fails alone, as it does in the reference's per-image loop
+    (encoder.py:120-135); with fail_fast the first failure is raised."""
+    status = T.prune_l1(dm, ratios, check=False).cpu().numpy()
+    for i in np.nonzero(status)[0]:
+        if not alive[i]:
+            continue
+        code = int(status[i])
+        cause = (StructuralError if code == ERR_STRUCTURAL else InvalidInputError)(
+            f"prune_l1 failed (status {code})")
+        if on_error == "fail_fast":
+            raise BatchItemError(int(i), cause)
+        alive[i] = cause
+
+
 def fit_round1_batch(images, cfg: EncodeConfig, seeds=None, device="cuda", on_error="fail_fast"):
     """Round 1 for every image: (DeviceModels, [EncodeReport])."""
     t0 = time.perf_counter()
@@ -240,7 +256,7 @@ def fit_full_batch(images, cfg: EncodeConfig, seeds=None, device="cuda", on_erro
     dm, reports, alive = fit_round1_batch(x, cfg, seeds, device, on_error)
     psnr = np.array([r.psnr_after_round[0] for r in reports])
     if not cfg.skip_round2:
-        T.prune_l1(dm, cfg.iterative_prune_ratio)
+        _prune_round(dm, cfg.iterative_prune_ratio, alive, on_error)
         pm = _psnr(dm, x, cfg.sin)
         _train_round(dm, x, cfg.retrain_lr, cfg.retrain_steps, cfg, reports, alive, on_error)
         psnr = _psnr(dm, x, cfg.sin)
@@ -249,12 +265,7 @@ def fit_full_batch(images, cfg: EncodeConfig, seeds=None, device="cuda", on_erro
             r.psnr_after_round.append(float(psnr[i]))
     sched = get_schedule(cfg.schedule)
     ratios = np.array([dynamic_ratio(sched, float(v)) if not math.isnan(v) else 0.0 for v in psnr])
-    status = T.prune_l1(dm, torch.from_numpy(ratios), check=False).cpu().numpy()
-    for i in np.nonzero(status)[0]:
-        err = BatchItemError(int(i), InvalidInputError(f"prune_l1 failed (status {status[i]})"))
-        if on_error == "fail_fast":
-            raise err
-        alive[i] = err.cause
+    _prune_round(dm, torch.from_numpy(ratios), alive, on_error)
     pm = _psnr(dm, x, cfg.sin)
     _train_round(dm, x, cfg.retrain_lr, cfg.retrain_steps, cfg, reports, alive, on_error)
     pf = _psnr(dm, x, cfg.sin)

@@ -34,13 +34,15 @@ class Store:
     def __init__(self, source, device=None, shard_rank: int = 0, shard_world: int = 1):
         if isinstance(source, (str, Path)):
             source = Path(source).read_bytes()
-        dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+        dev = torch.device("cuda") if device is None else torch.device(device)
         if dev.type != "cuda":
             raise InvalidInputError("Store lives in GPU memory; device must be a CUDA device")
+        if dev.index is None:  # "cuda" means the current device (e.g. after set_device(local_rank))
+            dev = torch.device("cuda", torch.cuda.current_device())
         self.device = dev
         arr = N.host_view(source)
         h = C.c_void_p()
-        N.check(N.lib().rinr_store_create(arr.ctypes.data if arr.size else None, arr.size, dev.index or 0,
+        N.check(N.lib().rinr_store_create(arr.ctypes.data if arr.size else None, arr.size, dev.index,
                                           shard_rank, shard_world, C.byref(h)))
         self._h = h
         info = N.StoreInfo()
