@@ -387,7 +387,7 @@ def run_ours(args, W):
     torch.cuda.current_stream().wait_stream(s)
     torch.cuda.synchronize()
     graph = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(graph):
+    with torch.cuda.graph(graph, stream=s):  # the stream warmed above (its decode workspaces exist)
         for k in range(K):
             step(Wu + k)
     graph.replay()

@@ -266,7 +266,7 @@ int launch_persist(const StoreView& sv, const int64_t* ids, int64_t n, const Dec
   lay.rec_bytes = (sv.max_slot_bytes + 16 + 15) & ~15;
   lay.pfx_words = (NL * 2 * KW + 3) & ~3;
   const bool shared_tab = a.aug == RINR_AUG_NONE;
-  const size_t fixed = size_t(NW) * 3 * NB * 16 * 4 + (shared_tab ? size_t(lay.tab_floats) * 4 : 0) + 64;
+  const size_t fixed = size_t(NW) * (3 * NB * 16 + 64) * 4 + (shared_tab ? size_t(lay.tab_floats) * 4 : 0) + 64;
   const size_t per_img = size_t(lay.net_words) * 4 + size_t(lay.rec_bytes) + size_t(lay.pfx_words) * 4 + 8 +
                          (shared_tab ? 0 : size_t(lay.tab_floats) * 4);
   constexpr int CPS = NW < 16 ? 16 / NW : 1;  // CTAs per SM
@@ -292,9 +292,10 @@ int launch_persist(const StoreView& sv, const int64_t* ids, int64_t n, const Dec
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   // development knob for timing breakdowns, compiled only with -DRINR_DEV_KNOBS (it
-  // produces wrong images): RINR_DEBUG_SKIP=1 skips phase 2, =2 the dequant, =3 both
+  // produces wrong images): RINR_DEBUG_SKIP=1 skips phase 2, =2 the dequant, =3 both,
+  // =4 everything after the CTA's work split (launch + PDL chain only)
 #ifdef RINR_DEV_KNOBS
-  static const int dbg = [] { const char* e = getenv("RINR_DEBUG_SKIP"); return e ? atoi(e) & 3 : 0; }();
+  static const int dbg = [] { const char* e = getenv("RINR_DEBUG_SKIP"); return e ? atoi(e) & 7 : 0; }();
 #else
   constexpr int dbg = 0;
 #endif
@@ -310,11 +311,25 @@ int launch_mode(const StoreView& sv, const int64_t* ids, int64_t n, const Decode
                 int32_t* status, cudaStream_t st, float omega, int flags) {
 #define RINR_LAUNCH(AL, ST, IB) \
   launch_persist<HID, NL, X3, ACC, NW, NB, Mode<AL, ST, IB>>(sv, ids, n, a, aug, out, status, st, omega, flags)
+#define RINR_LAUNCH_SEP(ST, IB) \
+  launch_persist<HID, NL, X3, ACC, NW, NB, Mode<true, ST, IB, true>>(sv, ids, n, a, aug, out, status, st, omega, flags)
   constexpr int GPX = NB * 16;
   if constexpr (ACC) {
     return RINR_LAUNCH(false, 0, false);  // accurate-sine kernels: one generic store path
   } else {
     if (a.out_w % GPX != 0) return RINR_LAUNCH(false, 0, false);
+    if constexpr (HID <= 16 && NB == 2) {
+      // one 32-pixel row per group: separable layer 0 (one sine per row per
+      // unit pair lane instead of one per pixel and unit)
+      if (a.out_w == GPX) {
+        const int st_mode = a.layout == RINR_LAYOUT_NCHW ? (a.dtype == RINR_OUT_F32 ? 1 : a.dtype == RINR_OUT_BF16 ? 2 : 0)
+                                                          : (a.dtype == RINR_OUT_F32 ? 3 : 0);
+        if (st_mode == 1) return sv.hidden_int8 ? RINR_LAUNCH_SEP(1, true) : RINR_LAUNCH_SEP(1, false);
+        if (st_mode == 2) return sv.hidden_int8 ? RINR_LAUNCH_SEP(2, true) : RINR_LAUNCH_SEP(2, false);
+        if (st_mode == 3) return sv.hidden_int8 ? RINR_LAUNCH_SEP(3, true) : RINR_LAUNCH_SEP(3, false);
+        return RINR_LAUNCH_SEP(0, false);  // u8 / other layouts: same pixels, scalar stores
+      }
+    }
     if (sv.hidden_int8) {  // store-wide: every hidden layer is affine8 codes
       if (a.layout == RINR_LAYOUT_NCHW && a.dtype == RINR_OUT_F32) return RINR_LAUNCH(true, 1, true);
       if (a.layout == RINR_LAYOUT_NCHW && a.dtype == RINR_OUT_BF16) return RINR_LAUNCH(true, 2, true);
@@ -326,6 +341,7 @@ int launch_mode(const StoreView& sv, const int64_t* ids, int64_t n, const Decode
     return RINR_LAUNCH(true, 0, false);
   }
 #undef RINR_LAUNCH
+#undef RINR_LAUNCH_SEP
 }
 
 template <int HID, int NL, bool X3, int T, bool INTB>
@@ -396,6 +412,9 @@ int launch_mma_t(const StoreView& sv, const int64_t* ids, int64_t n, const Decod
     // CTA shape = warps x (16-pixel blocks per warp): 16 x 2 measured best for
     // the [2,15,15,3] net against (8,4) (8,2) (16,1) (24,1) (32,1)
     // (8 x 2 at two CTAs per SM, so consecutive launches overlap: 2% slower; 20 x 2 at 92 registers: 5% slower)
+    // (a split prologue kernel dequantising the next batch beside the running
+    // decode did not pay: at <= 120 registers the 16-warp decode leaves room
+    // only for a 2-warp prologue, which took 13 us per batch)
     return launch_mode<HID, NL, X3, ACC, 16, 2>(sv, ids, n, a, aug, out, status, st, omega, flags);
   } else {
     if constexpr (!ACC) {

@@ -356,7 +356,7 @@ __device__ __forceinline__ void tc_reduce(const float* st, int rows, float* pw, 
 // fragment of n-tiles 0 / 1 is the A fragment of the next product, so
 //   z1 = a0 W1^T + b1,  out = a1 W2^T + b2,  d1 = (d2 W2) * c1,  d0 = (d1 W1) * c0
 // never leave registers.  Products are bf16 3-pass (Ah*Bh + Al*Bh + Ah*Bl,
-// truncation split: about 2^-16 relative per product), inside the MUFU mode's
+// round-to-nearest split: about 2^-17 relative per product), inside the MUFU mode's
 // stated gradient tolerance; the accurate-sine mode keeps the fp32 FFMA pass.
 // Layer 0 (K = 2) is FFMA in the same fragment layout.  C-fragment element e
 // of n-tile j: pixel row g + 8(e >> 1), unit 8j + 2tq + (e & 1).

@@ -13,7 +13,7 @@
 //     integer (code - zero_point) as the B operand — exact in bf16 — and apply
 //     f32(omega * scale) after the MMA, so the weights need no hi/lo split.
 //     Other layers use B = omega * w split into bf16 hi + lo.
-//   * X3 (precision FP32): A split into bf16 hi + lo, products
+//   * X3 (precision FP32): A split into bf16 hi + lo (both round-to-nearest), products
 //     Ah*Bh + Al*Bh (+ Ah*Bl for float B); max-abs vs the CPU oracle ~1e-5.
 //   * BF16: one pass.
 //   * Output layer: bias add + clamp in one saturating FADD (decoder.py:35).
@@ -30,6 +30,14 @@ __device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], 
       "{%0,%1,%2,%3};\n"
       : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
       : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// d = A * B (zero accumulator: the C operand is RZ, no register moves)
+__device__ __forceinline__ void mma16816_z(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm("mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%10,%10,%10,%10};\n"
+      : "=f"(d[0]), "=f"(d[1]), "=f"(d[2]), "=f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1), "f"(0.0f));
 }
 
 __device__ __forceinline__ uint32_t bf2_bits(__nv_bfloat162 v) { return *reinterpret_cast<uint32_t*>(&v); }
@@ -52,6 +60,14 @@ __device__ __forceinline__ float2 fadd2_(float2 a, float2 b) {
       : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
   return d;
 }
+__device__ __forceinline__ float2 fmul2(float2 a, float2 b) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2,%3};\n\tmov.b64 rb, {%4,%5};\n\t"
+      "mul.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0,%1}, rd;}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
 __device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
   float2 d;
   asm("{.reg .b64 ra, rb, rd;\n\tmov.b64 ra, {%2,%3};\n\tmov.b64 rb, {%4,%5};\n\t"
@@ -61,19 +77,21 @@ __device__ __forceinline__ float2 fsub2(float2 a, float2 b) {
   return d;
 }
 
-// (x0, x1) -> packed bf16x2 hi and, for the split, lo = bf16(x - f32(hi)).
-// X3 uses a truncation split: hi = top 16 bits (one byte-permute packs the
-// pair), lo = the exact remainder x - hi rounded to bf16; |x - hi - lo| <= 2^-16 |x|.
+// (x0, x1) -> packed bf16x2 hi = RN(x) and, for the split, lo = RN(x - hi):
+// |x - hi - lo| <= 2^-18 |x|.  Four instructions per pair: F2FP packs hi,
+// two FHFMA.BF16 form x - hi exactly in f32 straight from the packed bf16
+// halves (the sm_100 mixed-precision fma.rn.f32.bf16, hi * -1 + x), F2FP packs lo.
 template <bool X3>
 __device__ __forceinline__ void pack_act(float x0, float x1, uint32_t& hi, uint32_t& lo) {
+  asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(hi) : "f"(x1), "f"(x0));
   if constexpr (X3) {
-    const uint32_t u0 = __float_as_uint(x0), u1 = __float_as_uint(x1);
-    hi = __byte_perm(u0, u1, 0x7632);
-    const float2 r = fsub2(make_float2(x0, x1),
-                           make_float2(__uint_as_float(u0 & 0xffff0000u), __uint_as_float(u1 & 0xffff0000u)));
-    lo = bf2_bits(__floats2bfloat162_rn(r.x, r.y));
-  } else {
-    hi = bf2_bits(__floats2bfloat162_rn(x0, x1));
+    float l0, l1;
+    const unsigned short neg_one = 0xBF80;  // bf16 -1.0, a loop-invariant register
+    asm("{.reg .b16 h0, h1;\n\tmov.b32 {h0, h1}, %2;\n\t"
+        "fma.rn.f32.bf16 %0, h0, %5, %3;\n\tfma.rn.f32.bf16 %1, h1, %5, %4;}"
+        : "=f"(l0), "=f"(l1)
+        : "r"(hi), "f"(x0), "f"(x1), "h"(neg_one));
+    asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(lo) : "f"(l1), "f"(l0));
   }
 }
 

@@ -95,6 +95,88 @@ struct ImgRegs {
   }
 };
 
+// One fragment-owner dequant task of one record (slot = the record's shared
+// copy: layer-offset header, then the body at sv.hdr_bytes): h = 0 writes
+// layer 0 + the output layer, h = 1..NL-2 hidden layer h, straight into the
+// MMA operand layout of `net` (shared or global memory).  Every lane writes
+// exactly the fragment words it owns, padding included (no zero fill), with
+// values bit-exact to archive.materialize (archive.py:278-325).
+template <int HID, int NL, bool INTB>
+__device__ __forceinline__ void frag_task(const StoreView& sv, const uint8_t* slot, int h, NetView<HID, NL> net,
+                                          float omega, int lane) {
+  using C = MmaCfg<HID, NL>;
+  const uint32_t* lo = reinterpret_cast<const uint32_t*>(slot);
+  const uint8_t* rec = slot + sv.hdr_bytes;
+  if (h == 0) {
+    const DLayer L0 = parse_layer(rec, lo[0], lo[1], 2, HID);
+    const DLayer LO = parse_layer(rec, lo[NL - 1], lo[NL], HID, 3);
+    const WarpBits B0 = warp_bits(rec, L0, lane), BO = warp_bits(rec, LO, lane);
+    const ValueRecipe R0 = value_recipe(L0), RO = value_recipe(LO);
+    // layer 0: lane c -> {omega w[c][0], omega w[c][1], omega b[c], 0}
+    auto layer0 = [&](auto kind) {
+      constexpr int K = decltype(kind)::value;
+      const int c = lane < C::KP ? lane : 0;
+      const float w0 = value_at<false, K>(rec, R0, B0, c < HID ? 2 * c : 0);
+      const float w1 = value_at<false, K>(rec, R0, B0, c < HID ? 2 * c + 1 : 0);
+      if (lane < C::KP) {
+        float4 e = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (c < HID) {
+          e.x = __fmul_rn(omega, w0);
+          e.y = __fmul_rn(omega, w1);
+          e.z = __fmul_rn(omega, dq_bias(rec, L0, c));
+        }
+        reinterpret_cast<float4*>(net.l0)[c] = e;
+      }
+    };
+    const int k0 = value_kind(L0);
+    if (k0 == VK_F32) layer0(std::integral_constant<int, VK_F32>{});
+    else layer0(std::integral_constant<int, VK_GEN>{});
+    auto outl = [&](auto kind) {
+      constexpr int K = decltype(kind)::value;
+#pragma unroll
+      for (int t = 0; t < C::KT; ++t)
+        reinterpret_cast<uint4*>(net.fragO)[t * 32 + lane] =
+            frag_words<false, K>(rec, RO, BO, HID, 3, t, 0, 1.0f, lane);
+    };
+    const int ko = value_kind(LO);
+    if (ko == VK_F32) outl(std::integral_constant<int, VK_F32>{});
+    else outl(std::integral_constant<int, VK_GEN>{});
+    if (lane < 8) net.biasO[lane] = lane < 3 ? dq_bias(rec, LO, lane) : 0.0f;
+  } else {
+    const int l = h;
+    const DLayer L = parse_layer(rec, lo[l], lo[l + 1], HID, HID);
+    const WarpBits B = warp_bits(rec, L, lane);
+    const ValueRecipe R = value_recipe(L);
+    const bool int_b = INTB || int_b_exact(L);
+    uint4* fr = reinterpret_cast<uint4*>(net.fragH + (l - 1) * C::KT * C::NT * 32 * 4);
+    if (int_b) {
+#pragma unroll
+      for (int t = 0; t < C::KT; ++t)
+#pragma unroll
+        for (int j = 0; j < C::NT; ++j)
+          fr[(t * C::NT + j) * 32 + lane] = frag_words<true>(rec, R, B, HID, HID, t, j, omega, lane);
+    } else {
+      auto hid = [&](auto kind) {
+        constexpr int K = decltype(kind)::value;
+#pragma unroll
+        for (int t = 0; t < C::KT; ++t)
+#pragma unroll
+          for (int j = 0; j < C::NT; ++j)
+            fr[(t * C::NT + j) * 32 + lane] = frag_words<false, K>(rec, R, B, HID, HID, t, j, omega, lane);
+      };
+      if (value_kind(L) == VK_F32) hid(std::integral_constant<int, VK_F32>{});
+      else hid(std::integral_constant<int, VK_GEN>{});
+    }
+    static_assert(C::NT * 8 <= 32, "one bias entry per lane");
+    if (lane < C::NT * 8)
+      net.biasH[(l - 1) * C::NT * 8 + lane] = lane < HID ? __fmul_rn(omega, dq_bias(rec, L, lane)) : 0.0f;
+    if (lane == 0) {
+      net.modeH[l - 1] = int_b ? 1 : 0;
+      net.scaleH[l - 1] = int_b ? __double2float_rn(double(omega) * L.scale) : 1.0f;
+    }
+  }
+}
+
 // Phase-2 specialisation, chosen once per launch (warp-uniform):
 //   ALIGNED : out_w is a multiple of the group width, so a group lies inside one
 //             image row and every group is full
@@ -104,12 +186,41 @@ struct ImgRegs {
 // kernel keeps ptxas from spilling).
 //   INTB    : every hidden layer of every record in the store is affine8
 //             (integer-code B operand; compile-time, no branch around mma.sync)
-template <bool ALIGNED_, int STORE_, bool INTB_ = false>
+//   SEP     : separable layer 0 (out_w == group width, narrow net, MUFU sine):
+//             sin(a x + r(y)) = sin(a x) cos(r) + cos(a x) sin(r), with the
+//             per-image column terms held in registers and the per-row terms
+//             computed once per row by the warp (one sine per lane)
+template <bool ALIGNED_, int STORE_, bool INTB_ = false, bool SEP_ = false>
 struct Mode {
   static constexpr bool ALIGNED = ALIGNED_;
   static constexpr int STORE = STORE_;
   static constexpr bool INTB = INTB_;
+  static constexpr bool SEP = SEP_;
 };
+
+// Column terms of the separable layer 0 for one image (SEP mode): the lane's
+// four pixel columns c = 16 bk + 8 h + g and four units u(q) = 2 tq + (q & 1)
+// + 8 (q >> 1): sa = sin(omega w0[u] x_c), ca = cos(omega w0[u] x_c); plus
+// this lane's row-term unit (lane & 15): omega w1, omega b (+ pi/2 on the
+// cosine lanes 16..31).
+struct SepRegs {
+  float sa[2][2][4], ca[2][2][4];
+  float w1, b1;
+  int slot;  // this lane's row-term slot (sep_row_slot)
+};
+
+// Row terms of one output row y for the separable layer 0: lane (u = lane & 15,
+// f = lane >> 4) evaluates sin(r_u + f pi/2), r_u = omega (w1[u] y + b[u]), and
+// stores it at [pair u/2][f][u&1] so that one 16-byte load returns
+// {sin r_2p, sin r_2p+1, cos r_2p, cos r_2p+1}.
+// (The cosine lanes carry pi/2 in S.b1.)
+__device__ __forceinline__ int sep_row_slot(int lane) {
+  const int u = lane & 15, f = lane >> 4;
+  return 4 * (u >> 1) + 2 * f + (u & 1);
+}
+__device__ __forceinline__ void sep_row_terms(const SepRegs& S, float y, float* rowt, int slot) {
+  rowt[slot] = __sinf(fmaf(S.w1, y, S.b1));
+}
 
 // Per-lane store addressing, fixed for a launch.
 struct StoreLane {
@@ -153,7 +264,10 @@ template <int HID, int NL, bool X3, bool ACCURATE, int NB, class M>
 __device__ __forceinline__ void decode_group(const NetView<HID, NL>& net, const ImgRegs<HID, NL>& R,
                                              const float* colx, const float* rowy, const DecodeArgs& a,
                                              void* __restrict__ out, int64_t img, int64_t obase, int pbase,
-                                             int rb, int cb, float* stage, const StoreLane& SL, int lane) {
+                                             int rb, int cb, float* stage, const StoreLane& SL, int lane,
+                                             const SepRegs& S, const float* rowt, float* rowt_next, bool next_row,
+                                             int64_t gofs) {
+  // gofs: element offset of this lane's vector store for the group (STORE 1-3)
   // (rb, cb): row / column of the group's first pixel
   using C = MmaCfg<HID, NL>;
   constexpr int GPX = NB * 16;
@@ -162,46 +276,75 @@ __device__ __forceinline__ void decode_group(const NetView<HID, NL>& net, const 
   const int W = a.out_w;
 
   uint32_t ah[NB][C::KT][4], al[NB][C::KT][4];
+  if constexpr (M::SEP) {
+    static_assert(C::KT == 1 && NB == 2, "separable layer 0: one k-tile, one 32-pixel row per group");
+    // row terms of this group's row (written one group ahead), then per
+    // pixel and unit s = sa * cos r + ca * sin r  (FMUL2 + FFMA2 per unit pair)
+    const float4 r0 = reinterpret_cast<const float4*>(rowt)[tq];      // units 2tq, 2tq+1
+    const float4 r1 = reinterpret_cast<const float4*>(rowt)[tq + 4];  // units 2tq+8, 2tq+9
+    // next row's terms overlap this group (visible after the closing __syncwarp)
+    if (next_row) sep_row_terms(S, rowy[rb + 1], rowt_next, S.slot);
 #pragma unroll
-  for (int bk = 0; bk < NB; ++bk) {
-    float xr[2], yr[2];
+    for (int bk = 0; bk < NB; ++bk) {
+      float v[2][4];
 #pragma unroll
-    for (int h = 0; h < 2; ++h) {
-      if constexpr (ALIGNED) {  // W a multiple of the group: the group lies inside one row
-        xr[h] = colx[cb + 16 * bk + 8 * h + g];
-        yr[h] = rowy[rb];
-      } else {
-        int c = cb + 16 * bk + 8 * h + g, r = rb;
-        while (c >= W) { c -= W; ++r; }
-        const bool inside = pbase + 16 * bk + 8 * h + g < a.hw;
-        xr[h] = colx[inside ? c : 0];
-        yr[h] = rowy[inside ? r : 0];
+      for (int h = 0; h < 2; ++h) {
+        const float2 lo = ffma2(make_float2(S.sa[bk][h][0], S.sa[bk][h][1]), make_float2(r0.z, r0.w),
+                                fmul2(make_float2(S.ca[bk][h][0], S.ca[bk][h][1]), make_float2(r0.x, r0.y)));
+        const float2 hi = ffma2(make_float2(S.sa[bk][h][2], S.sa[bk][h][3]), make_float2(r1.z, r1.w),
+                                fmul2(make_float2(S.ca[bk][h][2], S.ca[bk][h][3]), make_float2(r1.x, r1.y)));
+        v[h][0] = lo.x;
+        v[h][1] = lo.y;
+        v[h][2] = hi.x;
+        v[h][3] = hi.y;
       }
+      pack_act<X3>(v[0][0], v[0][1], ah[bk][0][0], al[bk][0][0]);
+      pack_act<X3>(v[1][0], v[1][1], ah[bk][0][1], al[bk][0][1]);
+      pack_act<X3>(v[0][2], v[0][3], ah[bk][0][2], al[bk][0][2]);
+      pack_act<X3>(v[1][2], v[1][3], ah[bk][0][3], al[bk][0][3]);
     }
+  } else {
 #pragma unroll
-    for (int t = 0; t < C::KT; ++t) {
-      float s[2][4];
+    for (int bk = 0; bk < NB; ++bk) {
+      float xr[2], yr[2];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const bool pad = 16 * t + 8 * (q >> 1) >= HID;  // whole slot is padding (compile time)
-        float4 w;
-        if constexpr (ImgRegs<HID, NL>::REG_IO) w = R.w0[t][q];
-        else w = reinterpret_cast<const float4*>(net.l0)[16 * t + 2 * tq + (q & 1) + 8 * (q >> 1)];
-        if constexpr (ALIGNED) {
-          // the whole group is one image row: omega*(w1*y + b) once per unit
-          const float yb = fmaf(w.y, yr[0], w.z);
-          const float2 z = ffma2(make_float2(xr[0], xr[1]), make_float2(w.x, w.x), make_float2(yb, yb));
-          s[0][q] = pad ? 0.0f : sine<ACCURATE>(z.x);
-          s[1][q] = pad ? 0.0f : sine<ACCURATE>(z.y);
+      for (int h = 0; h < 2; ++h) {
+        if constexpr (ALIGNED) {  // W a multiple of the group: the group lies inside one row
+          xr[h] = colx[cb + 16 * bk + 8 * h + g];
+          yr[h] = rowy[rb];
         } else {
-#pragma unroll
-          for (int h = 0; h < 2; ++h) s[h][q] = pad ? 0.0f : sine<ACCURATE>(fmaf(w.y, yr[h], fmaf(w.x, xr[h], w.z)));
+          int c = cb + 16 * bk + 8 * h + g, r = rb;
+          while (c >= W) { c -= W; ++r; }
+          const bool inside = pbase + 16 * bk + 8 * h + g < a.hw;
+          xr[h] = colx[inside ? c : 0];
+          yr[h] = rowy[inside ? r : 0];
         }
       }
-      pack_act<X3>(s[0][0], s[0][1], ah[bk][t][0], al[bk][t][0]);
-      pack_act<X3>(s[1][0], s[1][1], ah[bk][t][1], al[bk][t][1]);
-      pack_act<X3>(s[0][2], s[0][3], ah[bk][t][2], al[bk][t][2]);
-      pack_act<X3>(s[1][2], s[1][3], ah[bk][t][3], al[bk][t][3]);
+#pragma unroll
+      for (int t = 0; t < C::KT; ++t) {
+        float s[2][4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const bool pad = 16 * t + 8 * (q >> 1) >= HID;  // whole slot is padding (compile time)
+          float4 w;
+          if constexpr (ImgRegs<HID, NL>::REG_IO) w = R.w0[t][q];
+          else w = reinterpret_cast<const float4*>(net.l0)[16 * t + 2 * tq + (q & 1) + 8 * (q >> 1)];
+          if constexpr (ALIGNED) {
+            // the whole group is one image row: omega*(w1*y + b) once per unit
+            const float yb = fmaf(w.y, yr[0], w.z);
+            const float2 z = ffma2(make_float2(xr[0], xr[1]), make_float2(w.x, w.x), make_float2(yb, yb));
+            s[0][q] = pad ? 0.0f : sine<ACCURATE>(z.x);
+            s[1][q] = pad ? 0.0f : sine<ACCURATE>(z.y);
+          } else {
+#pragma unroll
+            for (int h = 0; h < 2; ++h) s[h][q] = pad ? 0.0f : sine<ACCURATE>(fmaf(w.y, yr[h], fmaf(w.x, xr[h], w.z)));
+          }
+        }
+        pack_act<X3>(s[0][0], s[0][1], ah[bk][t][0], al[bk][t][0]);
+        pack_act<X3>(s[1][0], s[1][1], ah[bk][t][1], al[bk][t][1]);
+        pack_act<X3>(s[0][2], s[0][3], ah[bk][t][2], al[bk][t][2]);
+        pack_act<X3>(s[1][2], s[1][3], ah[bk][t][3], al[bk][t][3]);
+      }
     }
   }
   // ---- hidden layers ---------------------------------------------------------
@@ -210,13 +353,7 @@ __device__ __forceinline__ void decode_group(const NetView<HID, NL>& net, const 
     const uint32_t* fr = net.fragH + hl * C::KT * C::NT * 32 * 4;
     const bool int_b = M::INTB || (C::NH == 1 ? R.int1 : net.modeH[hl] != 0);
     const float sc = C::NH == 1 ? R.sc1 : net.scaleH[hl];
-    float acc[NB][C::NT][4];
-#pragma unroll
-    for (int bk = 0; bk < NB; ++bk)
-#pragma unroll
-      for (int j = 0; j < C::NT; ++j)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) acc[bk][j][e] = 0.0f;
+    float acc[NB][C::NT][4];  // first k-tile's MMA starts from zero (RZ accumulator)
     // int_b is warp-uniform: two straight-line MMA sequences instead of a
     // predicated mma.sync (which would still issue and force warp syncs)
     auto mma_layer = [&](auto with_lo) {
@@ -229,7 +366,8 @@ __device__ __forceinline__ void decode_group(const NetView<HID, NL>& net, const 
           else bf = reinterpret_cast<const uint4*>(fr)[(t * C::NT + j) * 32 + lane];
 #pragma unroll
           for (int bk = 0; bk < NB; ++bk) {
-            mma16816(acc[bk][j], ah[bk][t], bf.x, bf.y);
+            if (t == 0) mma16816_z(acc[bk][j], ah[bk][t], bf.x, bf.y);
+            else mma16816(acc[bk][j], ah[bk][t], bf.x, bf.y);
             if constexpr (X3) mma16816(acc[bk][j], al[bk][t], bf.x, bf.y);
             if constexpr (decltype(with_lo)::value) mma16816(acc[bk][j], ah[bk][t], bf.z, bf.w);
           }
@@ -276,27 +414,20 @@ __device__ __forceinline__ void decode_group(const NetView<HID, NL>& net, const 
   float ov[NB][4];
 #pragma unroll
   for (int bk = 0; bk < NB; ++bk) {
-    // three independent accumulators (hi*Bhi, hi*Blo, lo*Bhi): no dependent HMMA chain
-    float o[4] = {0.f, 0.f, 0.f, 0.f}, o2[4] = {0.f, 0.f, 0.f, 0.f}, o3[4] = {0.f, 0.f, 0.f, 0.f};
+    // one accumulator, hi*Bhi + lo*Bhi + hi*Blo chained (no combine adds)
+    float o[4];
 #pragma unroll
     for (int t = 0; t < C::KT; ++t) {
       uint4 bo;
       if constexpr (ImgRegs<HID, NL>::REG_IO) bo = R.bo[t];
       else bo = reinterpret_cast<const uint4*>(net.fragO)[t * 32 + lane];
-      mma16816(o, ah[bk][t], bo.x, bo.y);
-      mma16816(o2, ah[bk][t], bo.z, bo.w);
-      if constexpr (X3) mma16816(o3, al[bk][t], bo.x, bo.y);
+      if (t == 0) mma16816_z(o, ah[bk][t], bo.x, bo.y);
+      else mma16816(o, ah[bk][t], bo.x, bo.y);
+      if constexpr (X3) mma16816(o, al[bk][t], bo.x, bo.y);
+      mma16816(o, ah[bk][t], bo.z, bo.w);
     }
-    {
-      const float2 s01 = fadd2_(make_float2(o2[0], o2[1]), make_float2(o3[0], o3[1]));
-      const float2 s23 = fadd2_(make_float2(o2[2], o2[3]), make_float2(o3[2], o3[3]));
-      const float2 t01 = fadd2_(make_float2(o[0], o[1]), s01), t23 = fadd2_(make_float2(o[2], o[3]), s23);
-      o[0] = t01.x;
-      o[1] = t01.y;
-      o[2] = t23.x;
-      o[3] = t23.y;
-    }
-    // o[0]=(px g, ch 2tq) o[1]=(g, 2tq+1) o[2]=(g+8, 2tq) o[3]=(g+8, 2tq+1)
+    // o[0]=(px g, ch 2tq) o[1]=(g, 2tq+1) o[2]=(g+8, 2tq) o[3]=(g+8, 2tq+1);
+    // bias add + clamp (decoder.py:35) in one saturating FADD
 #pragma unroll
     for (int e = 0; e < 4; ++e) ov[bk][e] = __saturatef(o[e] + ((e & 1) ? R.bias_o1 : R.bias_o0));
   }
@@ -317,7 +448,7 @@ __device__ __forceinline__ void decode_group(const NetView<HID, NL>& net, const 
   if constexpr (M::STORE == 1) {
     if (SL.active) {
       const float4 v = *reinterpret_cast<const float4*>(stage + SL.soff[0]);
-      *reinterpret_cast<float4*>(static_cast<float*>(out) + obase + SL.goff + pbase) = v;
+      *reinterpret_cast<float4*>(static_cast<float*>(out) + gofs) = v;
     }
   } else if constexpr (M::STORE == 2) {
     if (SL.active) {
@@ -328,11 +459,11 @@ __device__ __forceinline__ void decode_group(const NetView<HID, NL>& net, const 
       pk.y = bf2_bits(__floats2bfloat162_rn(u.z, u.w));
       pk.z = bf2_bits(__floats2bfloat162_rn(w.x, w.y));
       pk.w = bf2_bits(__floats2bfloat162_rn(w.z, w.w));
-      *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(out) + obase + SL.goff + pbase) = pk;
+      *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(out) + gofs) = pk;
     }
   } else if constexpr (M::STORE == 3) {
     if (SL.active)
-      *reinterpret_cast<float4*>(static_cast<float*>(out) + obase + SL.goff + int64_t(pbase) * 3) =
+      *reinterpret_cast<float4*>(static_cast<float*>(out) + gofs) =
           make_float4(stage[SL.soff[0]], stage[SL.soff[1]], stage[SL.soff[2]], stage[SL.soff[3]]);
   } else {
     for (int i = lane; i < 3 * GPX; i += 32) {
@@ -353,41 +484,90 @@ __device__ __forceinline__ void phase2_loop(const uint32_t* nets, const float* t
                                             int warp, int lane) {
   using Net = NetView<HID, NL>;
   constexpr int GPX = NB * 16;
+  constexpr int64_t GSTEP = M::STORE == 3 ? 3 * GPX : GPX;  // store offset advance per group (NHWC: x3)
   const StoreLane SL = make_store_lane<NB, M::STORE>(a, lane);
   // each warp takes a contiguous run of groups (few image changes per warp)
   const int cnt = ge - gs;
   const int w0g = gs + int((int64_t(cnt) * warp) / NW), w1g = gs + int((int64_t(cnt) * (warp + 1)) / NW);
   int i = w0g / gpi, within = w0g - i * gpi;
-  int rb = (within * GPX) / a.out_w, cb = within * GPX - rb * a.out_w;
   int cur = -1;
   ImgRegs<HID, NL> R;
   R.set_norm(a, lane);
   Net net(const_cast<uint32_t*>(nets));
-  int64_t obase = 0;
+  int64_t obase = 0, gofs = 0;
   const float* colx = tabs;
   const float* rowy = tabs;
+  SepRegs S;
+  float* rowt = stage + 3 * GPX;  // [2][32] row-term buffers (SEP)
+  if constexpr (M::SEP) {
+    // out_w == GPX: group `within` is output row `within`
+    S.slot = sep_row_slot(lane);
 #pragma unroll 1
-  for (int gg = w0g; gg < w1g; ++gg) {
-    if (i != cur) {
-      cur = i;
-      net = Net(const_cast<uint32_t*>(nets) + i * lay.net_words);
-      R.load(net, lane);
-      obase = (cimg + i) * 3 * int64_t(a.hw);
-      colx = shared_tab ? tabs : tabs + i * lay.tab_floats;
-      rowy = colx + ((a.out_w + 3) & ~3);
+    for (int gg = w0g; gg < w1g; ++gg) {
+      if (i != cur) {
+        cur = i;
+        net = Net(const_cast<uint32_t*>(nets) + i * lay.net_words);
+        R.load(net, lane);
+        obase = (cimg + i) * 3 * int64_t(a.hw);
+        gofs = obase + SL.goff + int64_t(within) * GSTEP;
+        colx = shared_tab ? tabs : tabs + i * lay.tab_floats;
+        rowy = colx + ((a.out_w + 3) & ~3);
+        const int g = lane >> 2, tq = lane & 3;
+        const float4 lr = reinterpret_cast<const float4*>(net.l0)[lane & 15];
+        S.w1 = lr.y;
+        S.b1 = (lane >> 4) ? lr.z + 1.57079632679489662f : lr.z;  // cosine lanes: sin(r + pi/2)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float w0 = net.l0[4 * (2 * tq + (q & 1) + 8 * (q >> 1))];
+#pragma unroll
+          for (int bk = 0; bk < 2; ++bk)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+              const float ax = w0 * colx[16 * bk + 8 * h + g];
+              S.sa[bk][h][q] = __sinf(ax);
+              S.ca[bk][h][q] = __cosf(ax);
+            }
+        }
+        sep_row_terms(S, rowy[within], rowt + 32 * (gg & 1), S.slot);
+        __syncwarp();
+      }
+      const bool next_row = within + 1 < gpi && gg + 1 < w1g;
+      decode_group<HID, NL, X3, ACCURATE, NB, M>(net, R, colx, rowy, a, out, cimg + i, obase, within * GPX, within,
+                                                 0, stage, SL, lane, S, rowt + 32 * (gg & 1),
+                                                 rowt + 32 * ((gg + 1) & 1), next_row, gofs);
+      gofs += GSTEP;
+      if (++within == gpi) {
+        within = 0;
+        ++i;
+      }
     }
-    decode_group<HID, NL, X3, ACCURATE, NB, M>(net, R, colx, rowy, a, out, cimg + i, obase, within * GPX, rb, cb,
-                                               stage, SL, lane);
-    cb += GPX;
-    while (cb >= a.out_w) {
-      cb -= a.out_w;
-      ++rb;
-    }
-    if (++within == gpi) {
-      within = 0;
-      rb = 0;
-      cb = 0;
-      ++i;
+  } else {
+    int rb = (within * GPX) / a.out_w, cb = within * GPX - rb * a.out_w;
+#pragma unroll 1
+    for (int gg = w0g; gg < w1g; ++gg) {
+      if (i != cur) {
+        cur = i;
+        net = Net(const_cast<uint32_t*>(nets) + i * lay.net_words);
+        R.load(net, lane);
+        obase = (cimg + i) * 3 * int64_t(a.hw);
+        gofs = obase + SL.goff + int64_t(within) * GSTEP;
+        colx = shared_tab ? tabs : tabs + i * lay.tab_floats;
+        rowy = colx + ((a.out_w + 3) & ~3);
+      }
+      decode_group<HID, NL, X3, ACCURATE, NB, M>(net, R, colx, rowy, a, out, cimg + i, obase, within * GPX, rb, cb,
+                                                 stage, SL, lane, S, rowt, rowt, false, gofs);
+      gofs += GSTEP;
+      cb += GPX;
+      while (cb >= a.out_w) {
+        cb -= a.out_w;
+        ++rb;
+      }
+      if (++within == gpi) {
+        within = 0;
+        rb = 0;
+        cb = 0;
+        ++i;
+      }
     }
   }
 }
@@ -431,9 +611,14 @@ __global__ void __launch_bounds__(NW * 32, (NW < 16 ? 16 / NW : 1))
   const uint32_t G1u = G0u + qg + (blockIdx.x < rg ? 1u : 0u);
   const int64_t G0 = G0u, G1 = G1u;
   if (G0u >= G1u) return;
+  if (overlap & 8) {  // RINR_DEBUG_SKIP=4 (development builds): launch + PDL chain only
+    pdl_wait();
+    pdl_trigger();
+    return;
+  }
   const int64_t img0 = G0u / uint32_t(gpi);
   const int nimg = int((G1u - 1) / uint32_t(gpi) - uint32_t(img0) + 1);
-  float* stage = stagebase + warp * (3 * GPX);
+  float* stage = stagebase + warp * (3 * GPX + 64);  // output stage + SEP row terms
   const float invW = 1.0f / float(a.out_w);
   if (shared_tab) build_coord_tables(a, aug, 0, tabs, tabs + ((a.out_w + 3) & ~3), tid, NT);
 
@@ -477,77 +662,8 @@ __global__ void __launch_bounds__(NW * 32, (NW < 16 ? 16 / NW : 1))
       for (int task = (overlap & 4) ? ni * TPI : warp; task < ni * TPI; task += NW) {
         const int i = task / TPI, h = task - i * TPI;
         if (metaid[i] < 0) continue;
-        const uint32_t* lo = reinterpret_cast<const uint32_t*>(recs + size_t(i) * lay.rec_bytes);
-        const uint8_t* rec = recs + size_t(i) * lay.rec_bytes + sv.hdr_bytes;
-        Net net(nets + i * lay.net_words);
-        if (h == 0) {
-          const DLayer L0 = parse_layer(rec, lo[0], lo[1], 2, HID);
-          const DLayer LO = parse_layer(rec, lo[NL - 1], lo[NL], HID, 3);
-          const WarpBits B0 = warp_bits(rec, L0, lane), BO = warp_bits(rec, LO, lane);
-          const ValueRecipe R0 = value_recipe(L0), RO = value_recipe(LO);
-          // layer 0: lane c -> {omega w[c][0], omega w[c][1], omega b[c], 0}
-          auto layer0 = [&](auto kind) {
-            constexpr int K = decltype(kind)::value;
-            const int c = lane < C::KP ? lane : 0;
-            const float w0 = value_at<false, K>(rec, R0, B0, c < HID ? 2 * c : 0);
-            const float w1 = value_at<false, K>(rec, R0, B0, c < HID ? 2 * c + 1 : 0);
-            if (lane < C::KP) {
-              float4 e = make_float4(0.f, 0.f, 0.f, 0.f);
-              if (c < HID) {
-                e.x = __fmul_rn(omega, w0);
-                e.y = __fmul_rn(omega, w1);
-                e.z = __fmul_rn(omega, dq_bias(rec, L0, c));
-              }
-              reinterpret_cast<float4*>(net.l0)[c] = e;
-            }
-          };
-          const int k0 = value_kind(L0);
-          if (k0 == VK_F32) layer0(std::integral_constant<int, VK_F32>{});
-          else layer0(std::integral_constant<int, VK_GEN>{});
-          auto outl = [&](auto kind) {
-            constexpr int K = decltype(kind)::value;
-#pragma unroll
-            for (int t = 0; t < C::KT; ++t)
-              reinterpret_cast<uint4*>(net.fragO)[t * 32 + lane] =
-                  frag_words<false, K>(rec, RO, BO, HID, 3, t, 0, 1.0f, lane);
-          };
-          const int ko = value_kind(LO);
-          if (ko == VK_F32) outl(std::integral_constant<int, VK_F32>{});
-          else outl(std::integral_constant<int, VK_GEN>{});
-          if (lane < 8) net.biasO[lane] = lane < 3 ? dq_bias(rec, LO, lane) : 0.0f;
-        } else {
-          const int l = h;
-          const DLayer L = parse_layer(rec, lo[l], lo[l + 1], HID, HID);
-          const WarpBits B = warp_bits(rec, L, lane);
-          const ValueRecipe R = value_recipe(L);
-          const bool int_b = M::INTB || int_b_exact(L);
-          uint4* fr = reinterpret_cast<uint4*>(net.fragH + (l - 1) * C::KT * C::NT * 32 * 4);
-          if (int_b) {
-#pragma unroll
-            for (int t = 0; t < C::KT; ++t)
-#pragma unroll
-              for (int j = 0; j < C::NT; ++j)
-                fr[(t * C::NT + j) * 32 + lane] = frag_words<true>(rec, R, B, HID, HID, t, j, omega, lane);
-          } else {
-            auto hid = [&](auto kind) {
-              constexpr int K = decltype(kind)::value;
-#pragma unroll
-              for (int t = 0; t < C::KT; ++t)
-#pragma unroll
-                for (int j = 0; j < C::NT; ++j)
-                  fr[(t * C::NT + j) * 32 + lane] = frag_words<false, K>(rec, R, B, HID, HID, t, j, omega, lane);
-            };
-            if (value_kind(L) == VK_F32) hid(std::integral_constant<int, VK_F32>{});
-            else hid(std::integral_constant<int, VK_GEN>{});
-          }
-          static_assert(C::NT * 8 <= 32, "one bias entry per lane");
-          if (lane < C::NT * 8)
-            net.biasH[(l - 1) * C::NT * 8 + lane] = lane < HID ? __fmul_rn(omega, dq_bias(rec, L, lane)) : 0.0f;
-          if (lane == 0) {
-            net.modeH[l - 1] = int_b ? 1 : 0;
-            net.scaleH[l - 1] = int_b ? __double2float_rn(double(omega) * L.scale) : 1.0f;
-          }
-        }
+        frag_task<HID, NL, M::INTB>(sv, recs + size_t(i) * lay.rec_bytes, h, Net(nets + i * lay.net_words), omega,
+                                    lane);
       }
     }
     // Dequantise: one warp per (image, layer) task — the layer header is parsed

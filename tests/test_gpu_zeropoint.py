@@ -13,6 +13,7 @@ import numpy as np
 import pytest
 import torch
 
+from conftest import bf16_bar
 from oracle import rinr_oracle as O
 from paper_2306_16699_b200 import synth
 from paper_2306_16699_b200.compressor import quantize_batch
@@ -29,7 +30,11 @@ def _one_signed(arch, n, seed, frac_shifted):
     for l in range(1, len(arch.dims) - 2):
         w = mb.w[l]
         sign = np.where(rng.random(n) < 0.5, 1.0, -1.0).astype(np.float32)[:, None, None]
-        one = (np.abs(w) + np.float32(0.5) * np.abs(w).max(axis=(1, 2), keepdims=True)) * sign
+        # magnitudes in [0.1, 0.15] x max|w|: offset > spread, so zp ~ -510;
+        # small enough that the 10-layer net stays well conditioned (a
+        # one-signed layer at full SIREN scale amplifies f32 rounding ~15x per layer)
+        mx = np.abs(w).max(axis=(1, 2), keepdims=True)
+        one = (np.float32(0.1) * mx + np.float32(0.05) * np.abs(w)) * sign
         mb.w[l] = np.where(shifted[:, None, None], one, w).astype(np.float32)
     return quantize_batch(mb, "affine8"), shifted
 
@@ -57,5 +62,6 @@ def test_out_of_range_zero_point(arch_name, size, frac):
             err = float(np.abs(got - want).max())
             assert err <= 1e-3, (precision, err)
         got = st.decode(ids, size, size, layout="nhwc", precision="bf16").cpu().numpy()
+        bar = bf16_bar(arch.dims)
         for i in range(n):
-            assert O.psnr(got[i], want[i]) >= 50.0, i
+            assert O.psnr(got[i], want[i]) >= bar, (i, bar)
