@@ -23,6 +23,7 @@ EXPORTS = (
     "rinr_abi_version", "rinr_last_error", "rinr_last_error_record", "rinr_archive_validate", "rinr_archive_shard",
     "rinr_store_create", "rinr_store_destroy", "rinr_store_info", "rinr_store_record_meta",
     "rinr_dequantize", "rinr_decode", "rinr_prune_l1", "rinr_quantize", "rinr_psnr", "rinr_fit", "rinr_fit_render",
+    "rinr_serialize_size", "rinr_serialize_write",
 )
 
 
@@ -40,6 +41,16 @@ class StoreInfo(C.Structure):
 class FitParams(C.Structure):  # rinr_fit_params_t (include/rinr_b200_encoder.h)
     _fields_ = [("h", C.c_int32), ("w", C.c_int32), ("steps", C.c_int32), ("sin_mode", C.c_int32),
                 ("lr0", C.c_double), ("omega", C.c_double), ("curve_cap", C.c_int32), ("sched", C.c_void_p)]
+
+
+class SerializeArgs(C.Structure):  # rinr_serialize_args_t (include/rinr_b200_writer.h)
+    _fields_ = [
+        ("dims", C.POINTER(C.c_int32)), ("n_layers", C.c_int), ("n", C.c_int64),
+        ("source_h", C.c_uint32), ("source_w", C.c_uint32), ("omega", C.c_double), ("quant_bits", C.c_int),
+        ("d_w", C.c_void_p), ("d_mask", C.c_void_p), ("d_b", C.c_void_p), ("d_scale", C.c_void_p),
+        ("d_zp", C.c_void_p), ("d_const", C.c_void_p), ("d_codes", C.c_void_p),
+        ("id_prefix", C.c_char_p), ("first_id", C.c_int64), ("id_width", C.c_int),
+    ]
 
 
 class DecodeParams(C.Structure):
@@ -79,6 +90,8 @@ def lib() -> C.CDLL:
     L.rinr_psnr.argtypes = [vp, vp, i64, i64, C.c_int, vp, vp, vp]
     L.rinr_fit.argtypes = [vp, C.c_int, i64, vp, vp, vp, vp, C.POINTER(FitParams), vp, vp, vp, vp, vp, vp]
     L.rinr_fit_render.argtypes = [vp, C.c_int, i64, vp, vp, C.c_int32, C.c_int32, C.c_double, C.c_int32, vp, vp]
+    L.rinr_serialize_size.argtypes = [C.POINTER(SerializeArgs), vp, vp, vp, vp]
+    L.rinr_serialize_write.argtypes = [C.POINTER(SerializeArgs), vp, vp, vp, vp, vp, vp]
     L.rinr_diag_launch.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, vp, vp, C.POINTER(C.c_double)]
     L.rinr_diag_launch.restype = C.c_int
     for name in EXPORTS:

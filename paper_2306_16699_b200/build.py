@@ -19,8 +19,8 @@ ROOT = PKG.parent
 CSRC = PKG / "csrc"
 LIB_DIR = PKG / "_lib"
 LIB = LIB_DIR / "librinr_b200.so"
-SOURCES = [CSRC / "store.cpp", CSRC / "decode.cu", CSRC / "diag.cu", CSRC / "transforms.cu", CSRC / "fit.cu"]
-HEADERS = [ROOT / "include" / "rinr_b200.h", ROOT / "include" / "rinr_b200_diag.h", ROOT / "include" / "rinr_b200_transforms.h", ROOT / "include" / "rinr_b200_encoder.h", CSRC / "rinr_internal.h", CSRC / "device_common.cuh", CSRC / "mma_chain.cuh", CSRC / "persist.cuh", CSRC / "tc_decode.cuh"]
+SOURCES = [CSRC / "store.cpp", CSRC / "decode.cu", CSRC / "diag.cu", CSRC / "transforms.cu", CSRC / "fit.cu", CSRC / "writer.cu"]
+HEADERS = [ROOT / "include" / "rinr_b200.h", ROOT / "include" / "rinr_b200_diag.h", ROOT / "include" / "rinr_b200_transforms.h", ROOT / "include" / "rinr_b200_encoder.h", ROOT / "include" / "rinr_b200_writer.h", CSRC / "rinr_internal.h", CSRC / "device_common.cuh", CSRC / "mma_chain.cuh", CSRC / "persist.cuh", CSRC / "tc_decode.cuh"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -15,7 +15,7 @@ import numpy as np
 
 from . import net
 from .archive import serialize_batch
-from .compressor import ModelBatch, dynamic_ratio_cifar, prune_l1_batch, quantize_batch
+from .compressor import SCHEDULES, ModelBatch, dynamic_ratio_cifar, prune_l1_batch, quantize_batch
 from .net import Architecture
 
 ARCH_A = Architecture((2, 15, 15, 3))
@@ -54,8 +54,19 @@ def tweak_r1(mb: ModelBatch) -> ModelBatch:
 
 
 def cifar_ratios(n: int, seed: int) -> np.ndarray:
+    """Per-record prune ratios dynamic_ratio(cifar, U(28, 37) dB), vectorised
+    with the same IEEE operations as compressor.dynamic_ratio."""
     rng = np.random.default_rng(seed + 7919)
-    return np.array([dynamic_ratio_cifar(p) for p in rng.uniform(28.0, 37.0, n)])
+    p = rng.uniform(28.0, 37.0, n)
+    sched = SCHEDULES["cifar"]
+    out = np.where(p < sched.pieces[0][0], sched.below, sched.above)
+    done = np.zeros(n, bool)
+    for lo, hi, slope, intercept in sched.pieces:
+        done |= p < lo  # the reference loop breaks here
+        hit = ~done & (p <= hi)
+        out = np.where(hit, slope * p + intercept, out)
+        done |= hit
+    return out
 
 
 def config1(n: int = 256, variant: str = "R1") -> ModelBatch:
@@ -77,6 +88,47 @@ def config3(n: int = 256, seed: int = 0, arch: Architecture = ARCH_C, exact: boo
 
 def archive_bytes(mb: ModelBatch, start_id: int = 0) -> bytes:
     return serialize_batch(mb, record_ids(mb.n, start_id))
+
+
+def gpu_store_bytes(config: str, n: int, seed: int = 0, device="cuda", chunk: int = 1 << 18) -> bytes:
+    """Archive bytes of an n-record synthetic store of config 'c1', 'c2' or
+    'c3', generated on the GPU: net.init's distributions from a seeded torch
+    generator (R1 tweak), GPU prune_l1 to the config's ratios, GPU quantize
+    and the GPU writer (transforms.serialize) — the same pipeline as the host
+    generator, at GPU speed (a 1M-record c2 store in seconds)."""
+    import torch  # noqa: PLC0415
+
+    from . import transforms as T  # noqa: PLC0415
+    arch = {"c1": ARCH_A, "c2": ARCH_A, "c3": ARCH_C}[config]
+    src = (224, 224) if config == "c3" else (32, 32)
+    gen = torch.Generator(device=device).manual_seed(seed)
+    parts = []
+    lens = []
+    for s in range(0, n, chunk):
+        k = min(chunk, n - s)
+        ws, bs = [], []
+        dims = arch.dims
+        for li, (fi, fo) in enumerate(zip(dims[:-1], dims[1:])):
+            bound = 1.0 / fi if li == 0 else float(np.sqrt(6.0 / fi) / arch.omega)
+            ws.append(((torch.rand((k, fo * fi), generator=gen, device=device, dtype=torch.float64) * 2 - 1)
+                       * bound).to(torch.float32))
+            bs.append(torch.zeros((k, fo), device=device))
+        ws[-1] = ws[-1] * np.float32(20.0)  # R1: last layer x 20, bias 0.5
+        bs[-1] = torch.full_like(bs[-1], 0.5)
+        dm = T.DeviceModels(arch, torch.cat(ws, 1).contiguous(), torch.ones((k, sum(w.shape[1] for w in ws)),
+                            dtype=torch.uint8, device=device), torch.cat(bs, 1).contiguous(), src[0], src[1])
+        q = None
+        if config != "c1":
+            ratio = torch.from_numpy(cifar_ratios(k, seed + s)) if config == "c2" else 0.25
+            T.prune_l1(dm, ratio)
+            q = T.quantize(dm, "affine8")
+        buf = T.serialize(dm, q, id_prefix="img", first_id=s, id_width=8)
+        cnt = int(np.frombuffer(buf[6:10].cpu().numpy().tobytes(), "<u4")[0])
+        idx = buf[10:10 + 12 * cnt].cpu().numpy().view(np.dtype([("off", "<u8"), ("len", "<u4")]))
+        parts.append(buf[10 + 12 * cnt:].cpu().numpy())
+        lens.append(idx["len"].astype(np.int64))
+    from .archive import _wrap  # noqa: PLC0415
+    return _wrap(np.concatenate(parts), np.concatenate(lens))
 
 
 def large_store_bytes(config: str, n: int, seed: int = 0, chunk: int = 65536) -> bytes:

@@ -186,4 +186,45 @@ def psnr(a: torch.Tensor, b: torch.Tensor, quantized: bool = False):
     return mse, out
 
 
-__all__ = ["DeviceModels", "DeviceQuant", "prune_l1", "quantize", "quantized_batch", "psnr", "hidden_layer_indices"]
+def serialize(dm: DeviceModels, q: DeviceQuant | None = None, id_prefix: str = "img", first_id: int = 0,
+              id_width: int = 8) -> torch.Tensor:
+    """Archive bytes of the batch as a device uint8 tensor, written on the GPU
+    (csrc/writer.cu) and byte-identical to ``archive.serialize_batch`` of the
+    same models (the reference writer, archive.py:92-184).  Record k's id is
+    ``f"{id_prefix}{first_id + k:0{id_width}d}"``; ``q`` is the result of
+    ``quantize`` on these models (None: unquantised f32 records)."""
+    dev = dm.w.device
+    n = dm.n
+    dims, nl = _dims(dm.arch)
+    a = N.SerializeArgs()
+    a.dims = C.cast(dims, C.POINTER(C.c_int32))
+    a.n_layers = nl
+    a.n = n
+    a.source_h, a.source_w = int(dm.source_h), int(dm.source_w)
+    a.omega = float(dm.arch.omega)
+    a.quant_bits = q.bits if q is not None else 0
+    a.d_w, a.d_mask, a.d_b = dm.w.data_ptr(), dm.mask.data_ptr(), dm.b.data_ptr()
+    if q is not None:
+        a.d_scale, a.d_zp = q.scale.data_ptr(), q.zero_point.data_ptr()
+        const_u8 = q.constant.to(torch.uint8).contiguous()
+        a.d_const, a.d_codes = const_u8.data_ptr(), q.codes.data_ptr()
+    a.id_prefix = id_prefix.encode("utf-8")
+    a.first_id = int(first_id)
+    a.id_width = int(id_width)
+    rec_len = torch.empty(n, dtype=torch.int64, device=dev)
+    forms = torch.empty((n, nl), dtype=torch.uint8, device=dev)
+    kept = torch.empty((n, nl), dtype=torch.int32, device=dev)
+    with torch.cuda.device(dev):
+        st = _stream(dev)
+        N.check(N.lib().rinr_serialize_size(C.byref(a), rec_len.data_ptr(), forms.data_ptr(), kept.data_ptr(), st))
+        ends = torch.cumsum(rec_len, 0)
+        total = int(ends[-1].item()) if n else 0
+        rec_off = ends - rec_len
+        out = torch.empty(10 + 12 * n + total, dtype=torch.uint8, device=dev)
+        N.check(N.lib().rinr_serialize_write(C.byref(a), rec_off.data_ptr(), rec_len.data_ptr(), forms.data_ptr(),
+                                             kept.data_ptr(), out.data_ptr(), st))
+    return out
+
+
+__all__ = ["DeviceModels", "DeviceQuant", "prune_l1", "quantize", "quantized_batch", "psnr", "serialize",
+           "hidden_layer_indices"]

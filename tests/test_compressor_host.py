@@ -66,3 +66,12 @@ def test_prune_scope_errors():
     # per-layer: each matrix keeps ceil((1 - r) * size) entries
     p = compressor.prune_l1_batch(mb, 0.5, "per_layer")
     assert [int(x.sum()) for x in p.mask] == [4, 6]
+
+
+def test_cifar_ratios_vectorised():
+    """synth.cifar_ratios == dynamic_ratio(cifar, psnr) per record (compressor.py:50-65)."""
+    from paper_2306_16699_b200 import synth
+    from paper_2306_16699_b200.compressor import dynamic_ratio_cifar
+    rng = np.random.default_rng(11 + 7919)
+    want = np.array([dynamic_ratio_cifar(p) for p in rng.uniform(28.0, 37.0, 5000)])
+    np.testing.assert_array_equal(synth.cifar_ratios(5000, 11).view(np.uint64), want.view(np.uint64))

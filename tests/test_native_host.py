@@ -15,7 +15,7 @@ from paper_2306_16699_b200 import _native as N
 from paper_2306_16699_b200 import errors
 
 
-def header_symbols(names=("rinr_b200.h", "rinr_b200_transforms.h", "rinr_b200_encoder.h")):
+def header_symbols(names=("rinr_b200.h", "rinr_b200_transforms.h", "rinr_b200_encoder.h", "rinr_b200_writer.h")):
     text = "".join((ROOT / "include" / h).read_text() for h in names)
     return sorted(set(re.findall(r"RINR_API\s+[\w\s\*]+?\b(rinr_\w+)\s*\(", text)))
 
