@@ -1,35 +1,53 @@
 #!/usr/bin/env python
-"""Decode throughput bench (BASELINE.json metric: decoded images/sec).
+"""Decode throughput bench (BASELINE.json metric: decoded images/sec, 32x32
+and 224x224, % of the MUFU roofline).
 
-Workload (N=1 line = BASELINE config 2, the config the metric is quoted on):
-  c2: batch of 1024 records, 32x32 output, arch [2,15,15,3], each record
-      R1-initialised, L1-pruned to a per-record dynamic ratio (mean ~15%) and
-      affine8-quantised, held in an HBM store of --store-records records per
-      GPU (default 262,144 ~ 190 MB > 126 MB L2; each step samples a fresh
-      random batch of ids from it, so the records it reads are not L2-resident).
-  c3: batch of 256 records of arch [2,40x9,3] at 224x224 with random-resized-
-      crop + flip + ImageNet normalise, bf16 NCHW out (--config c3).
-A step = one fused decode launch over one batch (dequant prologue + MLP +
-epilogue).  `value` is device throughput with ids resident in HBM, timed with
-CUDA events around a CUDA-graph replay of exactly --steps launches, max over
-ranks.  `e2e` runs the same steps through the public API with host buffers:
-per step H2D of the ids from pinned memory, decode, D2H of the decoded
-ImageBuffer-layout (NHWC f32) batch into pinned memory.
+Default run (`python bench.py [--gpus N --steps K --warmup W]`): ONE JSON
+line whose headline is BASELINE configs[1] (c2), with the other two decode
+configs of the metric as sub-objects carrying the same keys:
+  c2 (headline): batch 1024, 32x32, arch [2,15,15,3], records R1-initialised,
+      L1-pruned to a per-record dynamic ratio (mean ~15%) and affine8-
+      quantised; fp32 NCHW out, precision 'fp32' (bf16x3 tensor-core split,
+      max-abs <= 1e-3 vs the reference).
+  "c1": configs[0], the reference's own CPU case: batch 256, 32x32, fp32
+      dense random-init (R1) records.
+  "c3": configs[2]: batch 256 of arch [2,40x9,3] (affine8, 25% pruned) at
+      224x224 with random-resized-crop + flip + ImageNet normalise, bf16 NCHW
+      out; credited at precision 'fp32' (bf16x3), precision 'bf16' beside it.
+Every store is larger than the 126 MB L2 (c2 262,144 records = 208 MB, c1
+262,144 = 366 MB, c3 16,384 = 223 MB per GPU) and every step decodes a fresh
+random batch of ids, so the records a step reads are not L2-resident.  The
+stores are generated on the GPU (synth.gpu_store_bytes: init + prune +
+quantize + the byte-exact GPU writer) and loaded through the public Store.
+
+A step = one fused decode launch over one batch (record fetch + bit-exact
+dequant prologue + MLP + epilogue).  `value` is device throughput with ids
+resident in HBM: CUDA events around one CUDA-graph replay of exactly --steps
+launches, after --warmup steps and ~0.5 s of replays that keep the clocks at
+their loaded state, max over ranks.  `e2e` runs the same steps through the
+public API with host buffers (per step: H2D of the ids from pinned memory,
+decode, D2H of the ImageBuffer-layout NHWC f32 batch).  `e2e_dropin` (c2)
+times the reference-API drop-in rinr.decode_batch(models, 32, 32) on host
+InrModels (serialise + store + decode + ImageBuffers).
 
 `--impl reference` times the reference algorithm on the host CPU instead
 (the numpy oracle port of rinr.decode_batch, oracle/rinr_oracle.py — the
-reference package itself cannot travel to the GPU box), with one worker
-process per core, over the same config and batch.
+reference package is pure Python and cannot travel to the GPU box), one
+worker process per core, on the same configs.
 
-Multi-GPU (torchrun): each rank holds its own shard of the store and decodes
-its own batch; there is no collective in the decode (scaling "weak").
+Multi-GPU (torchrun, one process per GPU): every rank generates the same
+world x R record archive and opens its shard with Store(..., shard_rank,
+shard_world) (records k % world == rank); each rank decodes its own batches
+with no collective (scaling "weak"); the barrier and the max-over-ranks
+timing reduction are the only NCCL calls.  `--config c4` / `c5`: ResNet-18
+training fed by the decode (c5: 1,048,576-record store sharded over the
+ranks, DDP gradient all-reduce over NCCL).
 """
 
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
 import subprocess
 import sys
@@ -55,7 +73,8 @@ def parse_args(argv=None):
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", choices=["c1", "c2", "c3", "c4", "c5"], default="c2")
     ap.add_argument("--precision", choices=["fp32", "bf16", "exact"], default=None)
-    ap.add_argument("--store-records", type=int, default=None)
+    ap.add_argument("--store-records", type=int, default=None, help="records per GPU")
+    ap.add_argument("--no-subs", action="store_true", help="headline config only (no c1 / c3 sub-objects)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-overlap", action="store_true",
@@ -64,28 +83,34 @@ def parse_args(argv=None):
 
 
 def workload(cfg: str):
-    if cfg in ("c4", "c5"):
-        return dict(batch=64, h=224, w=224, arch=[2] + [40] * 9 + [3], records=4096, desc=(
-            f"{cfg}: ResNet-18 training step (SGD lr 1e-2, wd 5e-4, bf16 autocast, channels_last; PAPER.md:446) "
-            "fed by on-the-fly decode of 64 affine8+25%-pruned [2,40x9,3] records per GPU at 224x224 with "
-            "random-resized-crop+flip+ImageNet normalise (bf16 NCHW)" +
-            (", DDP over NCCL, store sharded by record" if cfg == "c5" else "")))
+    if cfg == "c4":
+        return dict(batch=64, h=224, w=224, arch=[2] + [40] * 9 + [3], records=16384, classes=10, synth="c3",
+                    desc=("c4: ResNet-18 (10 classes) training step (SGD lr 1e-2 momentum 0.9, wd 5e-4, bf16 "
+                          "autocast, channels_last; PAPER.md:446) fed by on-the-fly decode of 64 affine8+25%-pruned "
+                          "[2,40x9,3] records per GPU at 224x224 with random-resized-crop+flip+ImageNet normalise "
+                          "(bf16 NCHW)"))
+    if cfg == "c5":
+        return dict(batch=128, h=32, w=32, arch=[2, 15, 15, 3], records=1 << 20, classes=10, synth="c2",
+                    desc=("c5: 1,048,576-record c2-style [2,15,15,3] store sharded over the GPUs (k % world), "
+                          "per-GPU decode of 128 records at 32x32 with CIFAR pad-4 crop+flip+normalise (bf16 NCHW) "
+                          "feeding ResNet-18 (10 classes, SGD lr 1e-2 momentum 0.9, wd 5e-4, bf16 autocast; "
+                          "PAPER.md:446), DDP gradient all-reduce over NCCL"))
     if cfg == "c1":
         return dict(batch=256, h=32, w=32, arch=[2, 15, 15, 3], records=262144, desc=(
             "c1: fp32 dense [2,15,15,3] random-init (R1) records, batch 256, 32x32, fp32 NCHW out"))
     if cfg == "c2":
         return dict(batch=1024, h=32, w=32, arch=[2, 15, 15, 3], records=262144, desc=(
             "c2: quantised(affine8)+pruned(mean~15%) [2,15,15,3] records, batch 1024, 32x32, fp32 NCHW out"))
-    return dict(batch=256, h=224, w=224, arch=[2] + [40] * 9 + [3], records=4096, desc=(
+    return dict(batch=256, h=224, w=224, arch=[2] + [40] * 9 + [3], records=16384, desc=(
         "c3: affine8 + 25%-pruned [2,40x9,3] records, batch 256, 224x224, random-resized-crop+flip+ImageNet "
         "normalise, bf16 NCHW out"))
 
 
-def store_bytes(cfg: str, n: int, seed: int) -> bytes:
+def host_store_bytes(cfg: str, n: int, seed: int) -> bytes:
+    """Small stores for the CPU legs (built before CUDA is initialised)."""
     from paper_2306_16699_b200 import synth
     if cfg == "c1":
-        mb = synth.tweak_r1(synth.random_batch(synth.ARCH_A, n, seed))
-        return synth.archive_bytes(mb)
+        return synth.archive_bytes(synth.tweak_r1(synth.random_batch(synth.ARCH_A, n, seed)))
     return synth.large_store_bytes(cfg, n, seed=seed)
 
 
@@ -169,7 +194,7 @@ def cpu_measure(cfg: str, W: dict, steps: int = None):
     (images/s, sample description, cores, per-step times)."""
     cores = host_cores()
     n_rec = 4096 if cfg != "c3" else 64
-    data = store_bytes(cfg, n_rec, seed=12345)
+    data = host_store_bytes(cfg, n_rec, seed=12345)
     pool = CpuPool(data, W["h"], W["w"], cores)
     rng = np.random.default_rng(0)
     B = W["batch"]
@@ -177,16 +202,15 @@ def cpu_measure(cfg: str, W: dict, steps: int = None):
         # calibrate: one warm batch
         ids = rng.integers(0, n_rec, B if cfg != "c3" else cores)
         aug = crop_params_np(len(ids), 0) if cfg == "c3" else None
-        t = pool.run(ids, aug)
-        per_img = t / len(ids)
+        pool.run(ids, aug)
         times = []
         if steps is None:  # bounded sample: ~10-30 s of CPU work across the cores
-            n = min(262144, cores * 8192) if cfg != "c3" else cores * 8
+            n = min(262144, cores * 8192) if cfg == "c2" else (min(65536, cores * 2048) if cfg == "c1" else cores * 8)
             ids = rng.integers(0, n_rec, n)
             aug = crop_params_np(n, 1) if cfg == "c3" else None
             t = pool.run(ids, aug)
             sample = (f"{n} images of {cfg} ({W['h']}x{W['w']}) decoded by the oracle port of rinr.decode_batch "
-                      f"(net.forward + clip{'+ crop/normalise' if cfg == 'c3' else ''}) from pre-materialised "
+                      f"(net.forward + clip{' + crop/flip/normalise' if cfg == 'c3' else ''}) from pre-materialised "
                       f"models, {cores} worker processes x 1 BLAS thread, {t:.2f} s wall")
             return n / t, sample, cores, [t]
         nb = B if cfg != "c3" else max(cores, 16)
@@ -201,24 +225,33 @@ def cpu_measure(cfg: str, W: dict, steps: int = None):
         pool.close()
 
 
-def run_reference(args, W):
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return 0
-    total = args.warmup + args.steps
-    _, sample, cores, times = cpu_measure(args.config, W, steps=total)
-    t = sum(times[args.warmup:])
-    per_step = W["batch"] if args.config != "c3" else max(cores, 16)
-    value = per_step * args.steps / t
-    line = {
-        "impl": "reference", "metric": "decoded images/sec", "value": value, "unit": "images/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * t / args.steps, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": W["desc"], "cpu": cpu_model()},
+def reference_entry(cfg: str, args, steps: int, warmup: int) -> dict:
+    W = workload(cfg)
+    _, sample, cores, times = cpu_measure(cfg, W, steps=warmup + steps)
+    t = sum(times[warmup:])
+    per_step = W["batch"] if cfg != "c3" else max(cores, 16)
+    value = per_step * steps / t
+    return {
+        "value": value, "unit": "images/s", "ms_per_step": 1e3 * t / steps, "steps": steps, "warmup": warmup,
+        "dtype": "f32", "config": {"workload": W["desc"], "cpu": cpu_model()},
         "cpu_baseline": {"value": value, "unit": "images/s", "cores": cores, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": "images/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    head = reference_entry(args.config, args, args.steps, args.warmup)
+    line = {"impl": "reference", "metric": "decoded images/sec", "value": head["value"], "unit": "images/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": head["ms_per_step"],
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic", "config": head["config"], "cpu_baseline": head["cpu_baseline"], "e2e": head["e2e"]}
+    if args.config == "c2" and not args.no_subs:
+        # the other legs of the metric, a few steps each (c3: ~0.1 s per 224^2 image per core)
+        line["c1"] = reference_entry("c1", args, min(args.steps, 10), min(args.warmup, 2))
+        line["c3"] = reference_entry("c3", args, min(args.steps, 3), 1)
     print(json.dumps(line), flush=True)
     return 0
 
@@ -312,46 +345,41 @@ def load_peaks():
         return {}
 
 
-def load_traffic(cfg):
+def load_traffic(cfg, precision):
+    """ncu DRAM bytes per launch of the config's decode kernel (profiles/)."""
     try:
         d = json.loads((ROOT / "profiles" / "ncu_summary.json").read_text())
-        return d.get(cfg, {}).get("dram_bytes_per_launch")
+        e = d.get(f"{cfg}_{precision}") or d.get(cfg) or {}
+        return e.get("dram_bytes_per_launch")
     except (OSError, ValueError):
         return None
 
 
-def run_ours(args, W):
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    cfg = args.config
-    precision = args.precision or ("bf16" if cfg == "c3" else "fp32")
-
-    # CPU baseline first (fork-based pool before CUDA is initialised).
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        ips, sample, cores, _ = cpu_measure(cfg, W)
-        cpu = {"value": ips, "unit": "images/s", "cores": cores, "kind": "port", "sample": sample}
-
-    import torch
-    torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from paper_2306_16699_b200 import Store, _native
-    from paper_2306_16699_b200.store import IMAGENET_MEAN, IMAGENET_STD, resized_crop_params
-
-    lib = _native.lib()
-    R = args.store_records or W["records"]
+def open_store(torch, cfg: str, W: dict, R: int, rank: int, world: int, local: int):
+    """Every rank generates the same world x R archive on its GPU and keeps
+    its shard (records k % world == rank) through the public Store."""
+    from paper_2306_16699_b200 import Store, synth
     t0 = time.perf_counter()
-    data = store_bytes(cfg, R, seed=1000 * rank)
-    st = Store(data, device=f"cuda:{local}")
-    build_s = time.perf_counter() - t0
+    data = synth.gpu_store_bytes(W.get("synth", cfg), R * world, seed=4242, device=f"cuda:{local}")
+    st = Store(data, device=f"cuda:{local}", shard_rank=rank, shard_world=world)
     del data
+    torch.cuda.synchronize()
+    return st, time.perf_counter() - t0
+
+
+def measure_decode(torch, dist, cfg: str, precision: str, args, rank: int, world: int, local: int, peaks: dict,
+                   st=None, build_s=None, with_e2e: bool = True) -> dict:
+    """One decode config on this rank's GPU: graph-timed value, roofline,
+    clocks and (optionally) e2e through the public API."""
+    from paper_2306_16699_b200.store import IMAGENET_MEAN, IMAGENET_STD, resized_crop_params
+    W = workload(cfg)
+    R = args.store_records if (args.store_records and cfg == args.config) else W["records"]
+    own = st is None
+    if own:
+        st, build_s = open_store(torch, cfg, W, R, rank, world, local)
     B, H, Wd = W["batch"], W["h"], W["w"]
     K, Wu = args.steps, args.warmup
-    gen = torch.Generator(device="cuda").manual_seed(rank)
+    gen = torch.Generator(device="cuda").manual_seed(1 + rank)
     ids = torch.randint(0, len(st), (Wu + K, B), device="cuda", generator=gen, dtype=torch.int64)
     if cfg == "c3":
         aug = [resized_crop_params(B, generator=torch.Generator().manual_seed(1000 * rank + s)).cuda()
@@ -369,35 +397,30 @@ def run_ours(args, W):
     def step(k):
         st.decode(ids[k], out=out, aug=aug[k], params=params, check=False)
 
-    # warm-up: W steps plus ~0.5 s so clocks reach their loaded state
     for k in range(Wu):
         step(k)
     torch.cuda.synchronize()
-    t_end = time.perf_counter() + 0.5
-    while time.perf_counter() < t_end:
-        for k in range(Wu):
-            step(k)
-        torch.cuda.synchronize()
-
-    # capture exactly K decode launches in one CUDA graph
+    # capture exactly K decode launches in one CUDA graph (on a warmed side stream)
     s = torch.cuda.Stream()
     s.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(s):
-        step(Wu)  # stream-side warm launch
+        step(Wu)
     torch.cuda.current_stream().wait_stream(s)
     torch.cuda.synchronize()
     graph = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(graph, stream=s):  # the stream warmed above (its decode workspaces exist)
+    with torch.cuda.graph(graph, stream=s):
         for k in range(K):
             step(Wu + k)
-    graph.replay()
-    torch.cuda.synchronize()
-
     sampler = ClockSampler(local)
     sampler.start()
-    time.sleep(0.25)
+    # keep the GPU busy ~0.5 s right up to the timed replay (loaded clocks, no idle gap)
+    t_end = time.perf_counter() + 0.5
+    while time.perf_counter() < t_end:
+        graph.replay()
+        torch.cuda.synchronize()
     if dist:
         dist.barrier()
+        graph.replay()  # re-warm after the barrier's host round trip
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -416,125 +439,215 @@ def run_ours(args, W):
         torch.cuda.synchronize()
         sustain.append(a0.elapsed_time(a1) * 1e-3)
     clocks = sampler.stop()
+    del graph
     elapsed_max = reduce_max(elapsed, dist, "cuda")
     value = world * B * K / elapsed_max
 
-    # e2e through the public API with host buffers
     e2e = None
-    if not args.no_e2e:
-        E = min(K, 50)
-        ids_host = ids[:E].cpu().pin_memory()
-        p_e2e = st.decode_params(H, Wd, dtype=torch.float32, layout="nhwc", precision=precision,
-                                 aug_mode="crop" if cfg == "c3" else None,
-                                 mean=IMAGENET_MEAN if cfg == "c3" else None,
-                                 std=IMAGENET_STD if cfg == "c3" else None)
-        aug_host = [a.cpu().pin_memory() if a is not None else None for a in aug[:E]]
-        # double-buffered device output; each step's D2H runs on two copy
-        # streams (halves of the batch, two DMA engines) while the next step's
-        # H2D + decode proceed on the main stream
-        out_dev = [torch.empty((B, H, Wd, 3), dtype=torch.float32, device="cuda") for _ in range(2)]
-        out_host = [torch.empty((B, H, Wd, 3), dtype=torch.float32).pin_memory() for _ in range(2)]
-        ids_dev = [torch.empty(B, dtype=torch.int64, device="cuda") for _ in range(2)]
-        aug_dev = [torch.empty((B, 5), dtype=torch.float32, device="cuda") for _ in range(2)]
-        cstreams = [torch.cuda.Stream(), torch.cuda.Stream()]
-        dec_done = [torch.cuda.Event() for _ in range(2)]
-        copy_done = [[torch.cuda.Event() for _ in range(2)] for _ in range(2)]
-        for sl in range(2):
-            for c in range(2):
-                copy_done[sl][c].record()
-        half = B // 2
-        main = torch.cuda.current_stream()
+    if with_e2e and not args.no_e2e:
+        e2e = measure_e2e(torch, dist, st, cfg, precision, ids, aug, B, H, Wd, K, world)
 
-        def e2e_step(k):
-            sl = k % 2
-            for c in range(2):
-                main.wait_event(copy_done[sl][c])  # out_dev[sl] / out_host[sl] free again
-            ids_dev[sl].copy_(ids_host[k], non_blocking=True)
-            a = None
-            if aug_host[k] is not None:
-                aug_dev[sl].copy_(aug_host[k], non_blocking=True)
-                a = aug_dev[sl]
-            st.decode(ids_dev[sl], out=out_dev[sl], aug=a, params=p_e2e, check=False)
-            dec_done[sl].record(main)
-            for c, (lo, hi) in enumerate(((0, half), (half, B))):
-                with torch.cuda.stream(cstreams[c]):
-                    cstreams[c].wait_event(dec_done[sl])
-                    out_host[sl][lo:hi].copy_(out_dev[sl][lo:hi], non_blocking=True)
-                    copy_done[sl][c].record(cstreams[c])
+    sines = B * H * Wd * HIDDEN_SUM[cfg]
+    dims = W["arch"]
+    hid_flops = 2.0 * H * Wd * sum(dims[i] * dims[i + 1] for i in range(1, len(dims) - 2)) * B
+    tensor_mult = 3 if precision == "fp32" else (1 if precision == "bf16" else 0)
+    mufu_peak = peaks.get("mufu_sin_per_s")
+    achieved = sines * K / elapsed
+    meas = load_peaks()
+    res = {
+        "value": value, "unit": "images/s", "ms_per_step": 1e3 * elapsed_max / K, "steps": K, "warmup": Wu,
+        "precision": precision,
+        "dtype": "f32" if precision == "exact" else "bf16x3" if precision == "fp32" else "bf16",
+        "config": {"workload": W["desc"], "precision": precision, "batch_per_gpu": B, "out": f"{H}x{Wd}",
+                   "store_records_per_gpu": len(st), "store_records_total": int(st.info.total_records),
+                   "store_bytes_per_gpu": int(st.info.device_bytes),
+                   "l2": "inputs larger than L2: each step decodes a fresh random batch from a store > 126 MB"
+                   if st.info.device_bytes > 126e6 else "store smaller than L2",
+                   "parallelism": f"image-sharded x{world} (Store shard k % {world}), no decode collective",
+                   "timing": "CUDA graph of K launches", "prologue_overlap": not args.no_overlap,
+                   "store_build_s": round(build_s, 2),
+                   "store_source": "GPU generator (synth.gpu_store_bytes) -> .rinr bytes -> Store"},
+        "roofline": {"bound": "mufu", "achieved": achieved / 1e9, "peak": mufu_peak / 1e9 if mufu_peak else None,
+                     "unit": "Gsin/s", "frac": achieved / mufu_peak if mufu_peak else None,
+                     "traffic": load_traffic(cfg, precision),
+                     "per_launch": {"sines": sines, "hidden_tensor_flops": hid_flops * max(tensor_mult, 1),
+                                    "algorithmic_sines_per_image": H * Wd * HIDDEN_SUM[cfg]},
+                     "peak_source": "measured in this run by a MUFU.SIN microbenchmark (rinr_diag_launch)",
+                     "tensor_frac_of_measured_bf16": (hid_flops * tensor_mult * K / elapsed) /
+                     (meas.get("bf16_tflops", 1652.1) * 1e12) if tensor_mult else 0.0},
+        "gpu_launches": K,
+        "clocks": clocks,
+        "sustain_ms_per_step": 1e3 * float(np.median(sustain)) / K if sustain else None,
+    }
+    if e2e:
+        res["e2e"] = e2e
+    if own:
+        st.close()
+    return res
 
-        for k in range(min(3, E)):
-            e2e_step(k)
+
+def measure_e2e(torch, dist, st, cfg, precision, ids, aug, B, H, Wd, K, world):
+    """Public API with host buffers: pinned ids in, NHWC f32 ImageBuffer batch out."""
+    from paper_2306_16699_b200.store import IMAGENET_MEAN, IMAGENET_STD
+    E = min(K, 50)
+    ids_host = ids[:E].cpu().pin_memory()
+    p_e2e = st.decode_params(H, Wd, dtype=torch.float32, layout="nhwc", precision=precision,
+                             aug_mode="crop" if cfg == "c3" else None,
+                             mean=IMAGENET_MEAN if cfg == "c3" else None,
+                             std=IMAGENET_STD if cfg == "c3" else None)
+    aug_host = [a.cpu().pin_memory() if a is not None else None for a in aug[:E]]
+    # double-buffered device output; each step's D2H runs on two copy streams
+    # (halves of the batch, two DMA engines) while the next step's H2D +
+    # decode proceed on the main stream
+    out_dev = [torch.empty((B, H, Wd, 3), dtype=torch.float32, device="cuda") for _ in range(2)]
+    out_host = [torch.empty((B, H, Wd, 3), dtype=torch.float32).pin_memory() for _ in range(2)]
+    ids_dev = [torch.empty(B, dtype=torch.int64, device="cuda") for _ in range(2)]
+    aug_dev = [torch.empty((B, 5), dtype=torch.float32, device="cuda") for _ in range(2)]
+    cstreams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    dec_done = [torch.cuda.Event() for _ in range(2)]
+    copy_done = [[torch.cuda.Event() for _ in range(2)] for _ in range(2)]
+    for sl in range(2):
+        for c in range(2):
+            copy_done[sl][c].record()
+    half = B // 2
+    main = torch.cuda.current_stream()
+
+    def e2e_step(k):
+        sl = k % 2
+        for c in range(2):
+            main.wait_event(copy_done[sl][c])  # out_dev[sl] / out_host[sl] free again
+        ids_dev[sl].copy_(ids_host[k], non_blocking=True)
+        a = None
+        if aug_host[k] is not None:
+            aug_dev[sl].copy_(aug_host[k], non_blocking=True)
+            a = aug_dev[sl]
+        st.decode(ids_dev[sl], out=out_dev[sl], aug=a, params=p_e2e, check=False)
+        dec_done[sl].record(main)
+        for c, (lo, hi) in enumerate(((0, half), (half, B))):
+            with torch.cuda.stream(cstreams[c]):
+                cstreams[c].wait_event(dec_done[sl])
+                out_host[sl][lo:hi].copy_(out_dev[sl][lo:hi], non_blocking=True)
+                copy_done[sl][c].record(cstreams[c])
+
+    for k in range(min(3, E)):
+        e2e_step(k)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    q0.record()
+    for k in range(E):
+        e2e_step(k)
+    for sl in range(2):  # the region ends when the last results are on the host
+        for c in range(2):
+            main.wait_event(copy_done[sl][c])
+    q1.record()
+    torch.cuda.synchronize()
+    et = reduce_max(q0.elapsed_time(q1) * 1e-3, dist, "cuda")
+    return {"value": world * B * E / et, "unit": "images/s",
+            "h2d_bytes_per_step": B * 8 + (B * 20 if cfg == "c3" else 0),
+            "d2h_bytes_per_step": B * H * Wd * 3 * 4, "steps": E,
+            "path": "Store.decode (C ABI rinr_decode) with pinned host ids in / NHWC f32 ImageBuffer batch out; "
+                    "D2H of step k on two copy streams overlaps step k+1's H2D + decode"}
+
+
+def measure_dropin(torch, n: int = 1024, reps: int = 3) -> dict:
+    """The reference-API drop-in: rinr.decode_batch(models, 32, 32) on host
+    InrModels of config c2 (decoder.py:39-61), wall-clock per call."""
+    from paper_2306_16699_b200 import decode_batch, synth
+    mb = synth.config2(n, seed=7, exact=False)
+    models = [mb.model(i) for i in range(n)]
+    decode_batch(models[:64], 32, 32)  # warm: library, allocator
+    times = []
+    for _ in range(reps):
         torch.cuda.synchronize()
-        if dist:
-            dist.barrier()
-        q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        q0.record()
-        for k in range(E):
-            e2e_step(k)
-        for sl in range(2):  # the region ends when the last results are on the host
-            for c in range(2):
-                main.wait_event(copy_done[sl][c])
-        q1.record()
-        torch.cuda.synchronize()
-        et = q0.elapsed_time(q1) * 1e-3
-        et = reduce_max(et, dist, "cuda")
-        e2e = {"value": world * B * E / et, "unit": "images/s", "h2d_bytes_per_step": B * 8 + (B * 20 if cfg == "c3"
-                                                                                           else 0),
-               "d2h_bytes_per_step": B * H * Wd * 3 * 4, "steps": E,
-               "path": "Store.decode (C ABI rinr_decode) with pinned host ids in / NHWC f32 ImageBuffer batch out; "
-                       "D2H of step k on two copy streams overlaps step k+1's H2D + decode"}
+        t0 = time.perf_counter()
+        imgs = decode_batch(models, 32, 32)
+        times.append(time.perf_counter() - t0)
+    assert len(imgs) == n and imgs[0].pixels.shape == (32, 32, 3)
+    t = float(np.median(times))
+    return {"value": n / t, "unit": "images/s", "models_per_call": n, "ms_per_call": 1e3 * t,
+            "path": "paper_2306_16699_b200.decode_batch (what install() binds to rinr.decode_batch): validate, "
+                    "group, serialise (vectorised writer), transient Store, one fused decode, ImageBuffers; "
+                    "host InrModels in, host ImageBuffers out, wall clock"}
 
-    peaks_meas = measure_peaks(torch, lib) if rank == 0 else {}
+
+def run_ours(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    head = args.config
+    subs = [] if (args.no_subs or head != "c2") else ["c1", "c3"]
+    precision = args.precision or "fp32"
+
+    # CPU baselines first (fork-based pool before CUDA is initialised), rank 0 at N=1 only
+    cpu = {}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        for cfg in [head] + subs:
+            ips, sample, cores, _ = cpu_measure(cfg, workload(cfg))
+            cpu[cfg] = {"value": ips, "unit": "images/s", "cores": cores, "kind": "port", "sample": sample}
+
+    import torch
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2306_16699_b200 import _native
+
+    lib = _native.lib()
+    peaks = measure_peaks(torch, lib)
+    res = {head: measure_decode(torch, dist, head, precision, args, rank, world, local, peaks)}
+    dropin = measure_dropin(torch) if (head == "c2" and rank == 0 and not args.no_e2e) else None
+    for cfg in subs:
+        if cfg == "c3":
+            W = workload(cfg)
+            st, build_s = open_store(torch, cfg, W, W["records"], rank, world, local)
+            r = measure_decode(torch, dist, cfg, "fp32", args, rank, world, local, peaks, st, build_s)
+            rb = measure_decode(torch, dist, cfg, "bf16", args, rank, world, local, peaks, st, build_s,
+                                with_e2e=False)
+            st.close()
+            r["bf16"] = {k: rb[k] for k in ("value", "ms_per_step", "roofline", "clocks", "dtype")}
+            r["bf16"]["parity"] = "per-image PSNR vs the reference decode >= 48 dB (10-layer nets, tests/conftest.py)"
+            res[cfg] = r
+        else:
+            res[cfg] = measure_decode(torch, dist, cfg, precision, args, rank, world, local, peaks)
     if dist:
         dist.barrier()
         dist.destroy_process_group()
     if rank != 0:
         return 0
 
-    sines = B * H * Wd * HIDDEN_SUM[cfg]
-    achieved = sines * K / elapsed
-    mufu_peak = peaks_meas.get("mufu_sin_per_s")
-    dims = W["arch"]
-    hid_flops = 2.0 * H * Wd * sum(dims[i] * dims[i + 1] for i in range(1, len(dims) - 2)) * B
-    tensor_mult = 3 if precision == "fp32" else (1 if precision == "bf16" else 0)
-    peaks = load_peaks()
+    h = res[head]
     line = {
-        "metric": "decoded images/sec", "value": value, "unit": "images/s", "n_gpus": world, "steps": K,
-        "warmup": Wu, "ms_per_step": 1e3 * elapsed_max / K, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f32" if precision == "exact" else "bf16x3" if precision == "fp32" else "bf16",
-        "data": "synthetic",
-        "config": {"workload": W["desc"], "precision": precision, "batch_per_gpu": B, "out": f"{H}x{Wd}",
-                   "store_records_per_gpu": R, "store_bytes_per_gpu": int(st.info.device_bytes),
-                   "l2": "inputs larger than L2: each step decodes a fresh random batch from a store > 126 MB"
-                   if st.info.device_bytes > 126e6 else "store smaller than L2",
-                   "parallelism": f"image-sharded x{world}, no decode collective", "timing": "CUDA graph of K launches",
-                   "prologue_overlap": not args.no_overlap,
-                   "store_build_s": round(build_s, 2)},
-        "roofline": {"bound": "mufu", "achieved": achieved / 1e9, "peak": mufu_peak / 1e9 if mufu_peak else None,
-                     "unit": "Gsin/s", "frac": achieved / mufu_peak if mufu_peak else None,
-                     "traffic": load_traffic(cfg),
-                     "per_launch": {"sines": sines, "hidden_tensor_flops": hid_flops * max(tensor_mult, 1)},
-                     "peak_source": "measured in this run by a MUFU.SIN microbenchmark (rinr_diag_launch)",
-                     "tensor_frac_of_measured_bf16": (hid_flops * tensor_mult * K / elapsed) /
-                     (peaks.get("bf16_tflops", 1669.7) * 1e12) if tensor_mult else 0.0,
-                     "measured_pipe_peaks": peaks_meas},
-        "gpu_launches": K,
-        "clocks": clocks,
-        "sustain_ms_per_step": 1e3 * float(np.median(sustain)) / K if sustain else None,
+        "metric": "decoded images/sec", "value": h["value"], "unit": "images/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": h["ms_per_step"], "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": h["dtype"], "data": "synthetic",
+        "config": h["config"], "roofline": h["roofline"], "gpu_launches": h["gpu_launches"],
+        "clocks": h["clocks"], "sustain_ms_per_step": h["sustain_ms_per_step"],
     }
-    if e2e:
-        line["e2e"] = e2e
-    if cpu:
-        line["cpu_baseline"] = cpu
+    line["roofline"]["measured_pipe_peaks"] = peaks
+    if "e2e" in h:
+        line["e2e"] = h["e2e"]
+    if dropin:
+        line["e2e_dropin"] = dropin
+    if head in cpu:
+        line["cpu_baseline"] = cpu[head]
+    for cfg in subs:
+        sub = res[cfg]
+        if cfg in cpu:
+            sub["cpu_baseline"] = cpu[cfg]
+        line[cfg] = sub
+        line["gpu_launches"] += sub["gpu_launches"] + sub.get("bf16", {}).get("gpu_launches", 0)
     print(json.dumps(line), flush=True)
-    st.close()
     return 0
 
 
-def run_train(args, W):
+def run_train(args):
     """C4 / C5: end-to-end ResNet-18 training fed by the fused decode."""
     import torch
     import torchvision
+    W = workload(args.config)
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -543,74 +656,40 @@ def run_train(args, W):
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    from paper_2306_16699_b200 import Store
-    from paper_2306_16699_b200.store import IMAGENET_MEAN, IMAGENET_STD, resized_crop_params
-
-    R = args.store_records or W["records"]
+    from paper_2306_16699_b200 import train
+    # c5: one 1M-record archive sharded over the ranks; c4: 16,384 records per GPU
+    total = args.store_records or (W["records"] if args.config == "c5" else W["records"] * world)
     t0 = time.perf_counter()
-    # every rank holds its own shard: records k with k % world == rank of a world*R store
-    st = Store(store_bytes("c3", R, seed=1000 * rank), device=f"cuda:{local}")
+    st = train.open_sharded_store(W["synth"], total, rank, world, device=f"cuda:{local}", seed=4242)
     build_s = time.perf_counter() - t0
-    B, H, Wd = W["batch"], W["h"], W["w"]
-    K, Wu = args.steps, args.warmup
     precision = args.precision or "bf16"
-    params = st.decode_params(H, Wd, dtype=torch.bfloat16, precision=precision, aug_mode="crop",
-                              mean=IMAGENET_MEAN, std=IMAGENET_STD)
-    model = torchvision.models.resnet18(num_classes=100).cuda().to(memory_format=torch.channels_last)
-    if dist:
-        model = torch.nn.parallel.DistributedDataParallel(model, device_ids=[local])
-    opt = torch.optim.SGD(model.parameters(), lr=1e-2, momentum=0.9, weight_decay=5e-4)
-    lossf = torch.nn.CrossEntropyLoss()
-    gen = torch.Generator(device="cuda").manual_seed(rank)
-    ids = torch.randint(0, len(st), (Wu + K, B), device="cuda", generator=gen)
-    labels = torch.randint(0, 100, (Wu + K, B), device="cuda", generator=gen)
-    aug = torch.stack([resized_crop_params(B, generator=torch.Generator().manual_seed(1000 * rank + s))
-                       for s in range(Wu + K)]).cuda()
-    xbuf = torch.empty((B, 3, H, Wd), dtype=torch.bfloat16, device="cuda").to(memory_format=torch.contiguous_format)
-
-    def train_step(x, y):
-        with torch.autocast("cuda", dtype=torch.bfloat16):
-            loss = lossf(model(x.contiguous(memory_format=torch.channels_last)), y)
-        opt.zero_grad(set_to_none=True)
-        loss.backward()
-        opt.step()
-        return loss
-
-    def step(k, decode=True):
-        if decode:
-            st.decode(ids[k], out=xbuf, aug=aug[k], params=params, check=False)
-        return train_step(xbuf, labels[k])
-
-    def timed(n0, n, decode=True):
-        if dist:
-            dist.barrier()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for k in range(n0, n0 + n):
-            loss = step(k, decode)
-        e1.record()
-        torch.cuda.synchronize()
-        return reduce_max(e0.elapsed_time(e1) * 1e-3, dist, "cuda"), float(loss.item())
-
-    for k in range(Wu):
-        step(k)
+    loop = train.DecodeTrainLoop(st, W["h"], W["w"], W["batch"], W["classes"], precision=precision,
+                                 aug="crop" if W["h"] == 224 else "offset", seed=rank,
+                                 ddp=dist is not None, device=f"cuda:{local}")
+    K, Wu = args.steps, args.warmup
+    for _ in range(Wu):
+        loop.step()
     torch.cuda.synchronize()
     sampler = ClockSampler(local)
     sampler.start()
-    elapsed, loss = timed(Wu, K)
+    t_end = time.perf_counter() + 0.3
+    while time.perf_counter() < t_end:
+        loop.step()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(K):
+        loss = loop.step()
+    e1.record()
+    torch.cuda.synchronize()
     clocks = sampler.stop()
-    value = world * B * K / elapsed
-    # decode alone (same launches) and the training step on a static pre-decoded batch
-    torch.cuda.synchronize()
-    d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    d0.record()
-    for k in range(Wu, Wu + K):
-        st.decode(ids[k], out=xbuf, aug=aug[k], params=params, check=False)
-    d1.record()
-    torch.cuda.synchronize()
-    dec_s = d0.elapsed_time(d1) * 1e-3
-    static_s, _ = timed(Wu, K, decode=False)
+    elapsed = reduce_max(e0.elapsed_time(e1) * 1e-3, dist, "cuda")
+    value = world * W["batch"] * K / elapsed
+    dec_s = reduce_max(loop.time_decode_only(K), dist, "cuda")
+    static_s = reduce_max(loop.time_train_only(K), dist, "cuda")
+    final_loss = float(loss.item())
     if dist:
         dist.destroy_process_group()
     if rank != 0:
@@ -619,13 +698,14 @@ def run_train(args, W):
         "metric": "decoded+trained images/sec", "value": value, "unit": "images/s", "n_gpus": world, "steps": K,
         "warmup": Wu, "ms_per_step": 1e3 * elapsed / K, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-        "config": {"workload": W["desc"], "batch_per_gpu": B, "store_records_per_gpu": R, "precision": precision,
-                   "parallelism": f"DDP x{world} (NCCL gradient all-reduce), image-sharded store" if world > 1
+        "config": {"workload": W["desc"], "batch_per_gpu": W["batch"], "store_records_per_gpu": len(st),
+                   "store_records_total": int(st.info.total_records), "precision": precision,
+                   "parallelism": f"DDP x{world} (NCCL gradient all-reduce), Store shard k % {world}" if world > 1
                    else "single GPU", "store_build_s": round(build_s, 2)},
         "decode_ms_per_step": 1e3 * dec_s / K,
         "decode_share_of_step": dec_s / elapsed,
-        "static_batch_images_per_s": world * B * K / static_s,
-        "final_loss": loss,
+        "static_batch_images_per_s": world * W["batch"] * K / static_s,
+        "final_loss": final_loss,
         "gpu_launches": K,
         "clocks": clocks,
     }
@@ -635,7 +715,6 @@ def run_train(args, W):
 
 def main(argv=None):
     args = parse_args(argv)
-    W = workload(args.config)
     if args.config in ("c4", "c5"):
         if args.impl == "reference":
             rank = int(os.environ.get("RANK", "0"))
@@ -643,10 +722,10 @@ def main(argv=None):
                 print(json.dumps({"impl": "reference", "unavailable": "the reference has no GPU training path "
                                   "(SPEC.md:8 puts ResNet-18 training out of scope)"}), flush=True)
             return 0
-        return run_train(args, W)
+        return run_train(args)
     if args.impl == "reference":
-        return run_reference(args, W)
-    return run_ours(args, W)
+        return run_reference(args)
+    return run_ours(args)
 
 
 if __name__ == "__main__":

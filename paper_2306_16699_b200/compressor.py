@@ -223,14 +223,21 @@ def to_half(model):
     return out
 
 
-def dequantize(model):
-    """Validate quantisation metadata and drop it (compressor.py:221-235)."""
+def check_quant(model) -> None:
+    """The metadata check of dequantize (compressor.py:229-232), without the copy."""
     if model.quant is None:
-        return model
+        return
     hidden = set(hidden_layer_indices(len(model.layers)))
     extra = set(model.quant.layers) - hidden
     if extra:
         raise FormatError(f"quantized_layers {sorted(extra)} are not hidden layers")
+
+
+def dequantize(model):
+    """Validate quantisation metadata and drop it (compressor.py:221-235)."""
+    if model.quant is None:
+        return model
+    check_quant(model)
     out = model.copy()
     out.quant = None
     return out
