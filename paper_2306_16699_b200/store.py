@@ -177,27 +177,32 @@ class Store:
 
 def pad_crop_params(n: int, pad: int = 4, generator: torch.Generator | None = None) -> torch.Tensor:
     """CIFAR-style RandomCrop(size, padding=pad) + horizontal flip: rows
-    {dx, dy, flip, pad, 0} with dx, dy ~ U{0..2*pad}, flip ~ Bernoulli(0.5)."""
+    {dx, dy, flip, pad, 0} with dx, dy ~ U{0..2*pad}, flip ~ Bernoulli(0.5).
+    Generated on the generator's device (a CUDA generator keeps a training
+    loop free of per-step host->device copies)."""
     g = generator
-    d = torch.randint(0, 2 * pad + 1, (n, 2), generator=g).float()
-    flip = torch.randint(0, 2, (n, 1), generator=g).float()
-    return torch.cat([d, flip, torch.full((n, 1), float(pad)), torch.zeros(n, 1)], 1)
+    dev = g.device if g is not None else None
+    d = torch.randint(0, 2 * pad + 1, (n, 2), generator=g, device=dev).float()
+    flip = torch.randint(0, 2, (n, 1), generator=g, device=dev).float()
+    return torch.cat([d, flip, torch.full((n, 1), float(pad), device=dev), torch.zeros(n, 1, device=dev)], 1)
 
 
 def resized_crop_params(n: int, scale=(0.08, 1.0), ratio=(3 / 4, 4 / 3),
                         generator: torch.Generator | None = None) -> torch.Tensor:
     """RandomResizedCrop + flip as continuous crop boxes in normalised source
     coordinates: rows {x0, y0, sx, sy, flip}.  The INR is sampled directly at
-    the crop's output grid, so no resampling happens."""
+    the crop's output grid, so no resampling happens.  Generated on the
+    generator's device."""
     g = generator
-    area = torch.empty(n).uniform_(scale[0], scale[1], generator=g)
-    logr = torch.empty(n).uniform_(float(np.log(ratio[0])), float(np.log(ratio[1])), generator=g)
+    dev = g.device if g is not None else None
+    area = torch.empty(n, device=dev).uniform_(scale[0], scale[1], generator=g)
+    logr = torch.empty(n, device=dev).uniform_(float(np.log(ratio[0])), float(np.log(ratio[1])), generator=g)
     r = torch.exp(logr)
     sx = torch.sqrt(area * r).clamp(max=1.0)
     sy = torch.sqrt(area / r).clamp(max=1.0)
-    x0 = torch.rand(n, generator=g) * (1.0 - sx)
-    y0 = torch.rand(n, generator=g) * (1.0 - sy)
-    flip = torch.randint(0, 2, (n,), generator=g).float()
+    x0 = torch.rand(n, generator=g, device=dev) * (1.0 - sx)
+    y0 = torch.rand(n, generator=g, device=dev) * (1.0 - sy)
+    flip = torch.randint(0, 2, (n,), generator=g, device=dev).float()
     return torch.stack([x0, y0, sx, sy, flip], 1)
 
 

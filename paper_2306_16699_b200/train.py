@@ -52,12 +52,14 @@ class DecodeTrainLoop:
         self.model = net
         self.opt = torch.optim.SGD(net.parameters(), lr=lr, momentum=0.9, weight_decay=weight_decay)
         self.lossf = torch.nn.CrossEntropyLoss()
-        self.host_gen = torch.Generator().manual_seed(seed)
+        # sampling and augmentation parameters are drawn on the device: a step
+        # issues no host->device copies and never waits on the host
+        self.gen = torch.Generator(device=self.dev).manual_seed(seed)
         n = len(store)
         rank, world = int(store.info.shard_rank), int(store.info.shard_world)
         glob = torch.arange(n, dtype=torch.int64) * world + rank  # global record index of local i
         self.labels_all = (glob % classes).to(self.dev)
-        self.perm = torch.empty(0, dtype=torch.int64)
+        self.perm = torch.empty(0, dtype=torch.int64, device=self.dev)
         self.pos = 0
         self.x = torch.empty((batch, 3, h, w), dtype=torch.bfloat16, device=self.dev)
 
@@ -65,7 +67,7 @@ class DecodeTrainLoop:
         """The next batch of local ids: a fresh permutation of the shard per epoch."""
         n = len(self.st)
         if self.pos + self.batch > self.perm.numel():
-            self.perm = torch.randperm(n, generator=self.host_gen)
+            self.perm = torch.randperm(n, generator=self.gen, device=self.dev)
             self.pos = 0
         ids = self.perm[self.pos:self.pos + self.batch]
         self.pos += self.batch
@@ -73,14 +75,12 @@ class DecodeTrainLoop:
 
     def next_aug(self) -> torch.Tensor:
         if self.aug == "crop":
-            return resized_crop_params(self.batch, generator=self.host_gen)
-        return pad_crop_params(self.batch, 4, generator=self.host_gen)
+            return resized_crop_params(self.batch, generator=self.gen)
+        return pad_crop_params(self.batch, 4, generator=self.gen)
 
     def decode(self, ids: torch.Tensor, aug: torch.Tensor) -> torch.Tensor:
-        ids_d = ids.to(self.dev, non_blocking=True)
-        aug_d = aug.to(self.dev, non_blocking=True)
-        self.st.decode(ids_d, out=self.x, aug=aug_d, params=self.params, check=False)
-        return self.labels_all[ids_d]
+        self.st.decode(ids, out=self.x, aug=aug, params=self.params, check=False)
+        return self.labels_all[ids]
 
     def train_on(self, x: torch.Tensor, y: torch.Tensor) -> torch.Tensor:
         with torch.autocast(self.dev.type, dtype=torch.bfloat16, enabled=self.dev.type == "cuda"):

@@ -303,6 +303,37 @@ def encoder_case():
     np.savez_compressed(OUT / "encoder.npz", **out)
 
 
+def fitted_case():
+    """INRs actually fitted by the reference encoder (encoder.fit_round1),
+    then compressed the paper's way (prune_l1 to the dynamic ratio or 25%,
+    quantize affine8), written by the reference writer.
+    Pins the PSNR against the SOURCE image of the reference decode of every
+    stored record, so the GPU decode's bf16 / fp32 paths can be held to
+    |PSNR(gpu, source) - PSNR(ref, source)| <= 0.05 dB."""
+    from rinr import encoder, metrics
+    from rinr.image import ImageBuffer
+    out = {}
+    sched = compressor.get_schedule("cifar")
+    for name, arch, n, size, steps in (("A", ARCH_A, 4, 32, 3000), ("C", ARCH_C, 2, 48, 600)):
+        imgs = test_images(n, size, size, seed=41 if name == "A" else 42)
+        models = []
+        for i in range(n):
+            cfg = encoder.EncodeConfig(arch, round1_steps=steps, seed=encoder.derive_seed(9, i))
+            m, rep = encoder.fit_round1(ImageBuffer(imgs[i]), cfg)
+            models.append(m)  # dense f32 as fitted
+            ratio = compressor.dynamic_ratio(sched, rep.psnr_after_round[0]) if name == "A" else 0.25
+            models.append(compressor.quantize(compressor.prune_l1(m, ratio), "affine8"))
+        data = build_archive(models)
+        recs = archive.read(io.BytesIO(data)).records
+        dec = decoder.decode_batch([r.model for r in recs])
+        src = np.repeat(imgs, 2, axis=0)  # record 2i, 2i+1 encode image i
+        out[f"{name}/archive"] = np.frombuffer(data, np.uint8)
+        out[f"{name}/source"] = src
+        out[f"{name}/decode"] = np.stack([d.pixels for d in dec])
+        out[f"{name}/psnr"] = np.array([metrics.psnr(d, ImageBuffer(s)).psnr_db for d, s in zip(dec, src)])
+    np.savez_compressed(OUT / "fitted.npz", **out)
+
+
 def _src(m, h=32, w=32):
     m.source_h, m.source_w = h, w
     return m
@@ -312,7 +343,10 @@ if __name__ == "__main__" and sys.argv[1:] == ["transforms"]:
     transforms_case()
 elif __name__ == "__main__" and sys.argv[1:] == ["encoder"]:
     encoder_case()
+elif __name__ == "__main__" and sys.argv[1:] == ["fitted"]:
+    fitted_case()
 elif __name__ == "__main__":
     main()
     transforms_case()
     encoder_case()
+    fitted_case()

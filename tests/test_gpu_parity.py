@@ -4,22 +4,25 @@ the reference's golden outputs.
 Tolerances (stated by north_star / SURVEY §8c):
   * dequantised weights      : bit-exact (uint32 compare) vs archive.materialize
   * precision 'exact', 'fp32': max-abs <= 1e-3 in [0,1] vs the reference decode
-  * precision 'bf16'         : per-image PSNR vs the reference decode >= 40 dB
-                               (inputs are R1 models whose last layer is scaled
-                               x20, which amplifies bf16 rounding ~20x)
+  * precision 'bf16'         : per-image PSNR vs the reference decode >= 55 dB
+                               for 3-layer nets, >= 48 dB for the 10-layer nets
+                               (conftest.bf16_bar; inputs are R1 models whose
+                               last layer is scaled x20, which amplifies bf16
+                               rounding ~20x); on reference-fitted INRs every
+                               precision keeps PSNR vs the source within
+                               0.05 dB (test_gpu_fitted.py)
 """
 
 import numpy as np
 import pytest
 import torch
 
-from conftest import STORE_CASES
+from conftest import STORE_CASES, bf16_bar
 from oracle import rinr_oracle as O
 
 pytestmark = pytest.mark.gpu
 
 FP32_TOL = 1e-3
-BF16_PSNR_DB = 40.0
 
 
 @pytest.fixture(scope="module")
@@ -49,6 +52,7 @@ def test_dequantize_bit_exact(golden, Store, case):
 @pytest.mark.parametrize("case", STORE_CASES)
 def test_decode_parity(golden, Store, case, precision, sin):
     g = golden(case)
+    models = O.read_models(g["archive"].tobytes())
     with Store(g["archive"].tobytes()) as st:
         for key in g:
             if not key.startswith("decode_"):
@@ -62,7 +66,7 @@ def test_decode_parity(golden, Store, case, precision, sin):
             if precision == "bf16":
                 for i in range(want.shape[0]):
                     p = O.psnr(got[i], want[i])
-                    assert p >= BF16_PSNR_DB, (key, i, p)
+                    assert p >= bf16_bar(models[i].dims), (key, i, p)
             else:
                 err = float(np.abs(got - want).max())
                 assert err <= FP32_TOL, (key, err)

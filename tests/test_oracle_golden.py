@@ -152,3 +152,15 @@ def test_training_oracle(golden):
     np.testing.assert_array_equal(curve, g["train/curve"])
     np.testing.assert_array_equal(np.concatenate([x.ravel() for x in ws]), g["train/w"])
     np.testing.assert_array_equal(np.concatenate([x.ravel() for x in bs]), g["train/b"])
+
+
+def test_fitted_oracle(golden):
+    """The oracle reproduces the reference decode of reference-fitted INRs
+    bit for bit, and its PSNR against the source images (metrics.py:23-41)."""
+    g = golden("fitted")
+    for name in ("A", "C"):
+        models = O.read_models(g[f"{name}/archive"].tobytes())
+        got = np.stack(O.decode_batch(models))
+        np.testing.assert_array_equal(got.view(np.uint32), g[f"{name}/decode"].view(np.uint32))
+        for i in range(len(models)):
+            assert abs(O.psnr(got[i], g[f"{name}/source"][i]) - g[f"{name}/psnr"][i]) <= 1e-9
