@@ -271,6 +271,10 @@ __global__ void __launch_bounds__(4 * T * 32, 1)
   __syncthreads();
   tc::fence_after();
   const uint32_t tmem_base = *tmem_slot;
+  // 16-byte vector stores of full warps: f32 NCHW / NHWC need hw % 4 == 0,
+  // bf16 NCHW hw % 8 == 0 (u8 and the rest store per value)
+  const bool vec_store = (a.dtype == RINR_OUT_F32 && a.hw % 4 == 0) ||
+                         (a.dtype == RINR_OUT_BF16 && a.layout == RINR_LAYOUT_NCHW && a.hw % 8 == 0);
   uint32_t mma_phase = 0;  // parity of this epilogue warp's slot mbarrier
 
   for (int c0 = 0; c0 < nimg; c0 += lay.maxi) {
@@ -499,18 +503,59 @@ __global__ void __launch_bounds__(4 * T * 32, 1)
         tc::tmem_ld8(tacc, o);
         tc::tmem_wait_ld();
         tc::fence_before();  // TMEM reads done before the next tile's MMA overwrites it
-        if (inside) {
+        // epilogue: clamp (decoder.py:35), normalise, then the warp's 32
+        // consecutive pixels x 3 channels go through a shared-memory stage
+        // (the free phase-1 scratch) and out as 16-byte vector stores
+        float* sw = reinterpret_cast<float*>(smem) + warp * 96;  // [ch][32 px]
 #pragma unroll
-          for (int ch = 0; ch < 3; ++ch) {
-            float vv = __saturatef(o[ch] + net.biasO[ch]);
-            if (!a.identity) {
-              const float m = ch == 0 ? a.mean[0] : (ch == 1 ? a.mean[1] : a.mean[2]);
-              const float sd = ch == 0 ? a.stdv[0] : (ch == 1 ? a.stdv[1] : a.stdv[2]);
-              vv = __fdiv_rn(__fsub_rn(vv, m), sd);
-            }
-            store_value(a, out, img, p, ch, vv);
+        for (int ch = 0; ch < 3; ++ch) {
+          float vv = __saturatef(o[ch] + net.biasO[ch]);
+          if (!a.identity) {
+            const float m = ch == 0 ? a.mean[0] : (ch == 1 ? a.mean[1] : a.mean[2]);
+            const float sd = ch == 0 ? a.stdv[0] : (ch == 1 ? a.stdv[1] : a.stdv[2]);
+            vv = __fdiv_rn(__fsub_rn(vv, m), sd);
           }
+          sw[ch * 32 + lane] = vv;
         }
+        __syncwarp();
+        const int p0 = p - lane;  // first pixel of the warp (a multiple of 32)
+        if (vec_store && p0 + 32 <= a.hw) {
+          if (a.layout == RINR_LAYOUT_NCHW && a.dtype == RINR_OUT_BF16) {
+            if (lane < 12) {  // channel lane/4, 8 pixels each
+              const int ch = lane >> 2, part = lane & 3;
+              const float4 u = *reinterpret_cast<const float4*>(sw + ch * 32 + part * 8);
+              const float4 v = *reinterpret_cast<const float4*>(sw + ch * 32 + part * 8 + 4);
+              uint4 pk;
+              pk.x = bf2_bits(__floats2bfloat162_rn(u.x, u.y));
+              pk.y = bf2_bits(__floats2bfloat162_rn(u.z, u.w));
+              pk.z = bf2_bits(__floats2bfloat162_rn(v.x, v.y));
+              pk.w = bf2_bits(__floats2bfloat162_rn(v.z, v.w));
+              *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(out) + (img * 3 + ch) * int64_t(a.hw) + p0 +
+                                        part * 8) = pk;
+            }
+          } else if (a.layout == RINR_LAYOUT_NCHW) {  // f32
+            if (lane < 24) {
+              const int ch = lane >> 3, part = lane & 7;
+              *reinterpret_cast<float4*>(static_cast<float*>(out) + (img * 3 + ch) * int64_t(a.hw) + p0 + part * 4) =
+                  *reinterpret_cast<const float4*>(sw + ch * 32 + part * 4);
+            }
+          } else {  // NHWC f32: 96 interleaved values
+            if (lane < 24) {
+              float v4[4];
+#pragma unroll
+              for (int k = 0; k < 4; ++k) {
+                const int e = 4 * lane + k, px = e / 3, ch = e - 3 * px;
+                v4[k] = sw[ch * 32 + px];
+              }
+              *reinterpret_cast<float4*>(static_cast<float*>(out) + (img * a.hw + p0) * 3 + 4 * lane) =
+                  make_float4(v4[0], v4[1], v4[2], v4[3]);
+            }
+          }
+        } else if (inside) {
+#pragma unroll
+          for (int ch = 0; ch < 3; ++ch) store_value(a, out, img, p, ch, sw[ch * 32 + lane]);
+        }
+        __syncwarp();
       }
     }
     tc::fence_before();
