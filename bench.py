@@ -572,10 +572,30 @@ def measure_dropin(torch, n: int = 1024, reps: int = 3) -> dict:
                     "host InrModels in, host ImageBuffers out, wall clock"}
 
 
-def run_ours(args):
+def dist_env():
+    """(rank, world, local GPU, backend).  RINR_BENCH_BACKEND=gloo with
+    RINR_BENCH_ONE_GPU=1 runs every rank on cuda:0 (the multi-rank test of
+    this script on a one-GPU box, tests/test_gpu_bench_multirank.py); real
+    runs use NCCL, one process per GPU."""
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = 0 if os.environ.get("RINR_BENCH_ONE_GPU") == "1" else int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local, os.environ.get("RINR_BENCH_BACKEND", "nccl")
+
+
+def init_dist(torch, world, local, backend):
+    if world <= 1:
+        return None
+    import torch.distributed as dist
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        dist.init_process_group(backend)
+    return dist
+
+
+def run_ours(args):
+    rank, world, local, backend = dist_env()
     head = args.config
     subs = [] if (args.no_subs or head != "c2") else ["c1", "c3"]
     precision = args.precision or "fp32"
@@ -589,10 +609,7 @@ def run_ours(args):
 
     import torch
     torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dist = init_dist(torch, world, local, backend)
     from paper_2306_16699_b200 import _native
 
     lib = _native.lib()
@@ -648,17 +665,14 @@ def run_train(args):
     import torch
     import torchvision
     W = workload(args.config)
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    rank, world, local, backend = dist_env()
     torch.cuda.set_device(local)
-    dist = None
-    if world > 1:
-        import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dist = init_dist(torch, world, local, backend)
     from paper_2306_16699_b200 import train
     # c5: one 1M-record archive sharded over the ranks; c4: 16,384 records per GPU
-    total = args.store_records or (W["records"] if args.config == "c5" else W["records"] * world)
+    # (--store-records: records per GPU)
+    total = args.store_records * world if args.store_records else (
+        W["records"] if args.config == "c5" else W["records"] * world)
     t0 = time.perf_counter()
     st = train.open_sharded_store(W["synth"], total, rank, world, device=f"cuda:{local}", seed=4242)
     build_s = time.perf_counter() - t0

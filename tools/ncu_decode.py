@@ -27,7 +27,8 @@ def main():
     ap.add_argument("--batch", type=int, default=None)
     a = ap.parse_args()
     W = bench.workload(a.config)
-    st = Store(bench.store_bytes(a.config, a.records, seed=0))
+    from paper_2306_16699_b200 import synth
+    st = Store(synth.gpu_store_bytes(a.config, a.records, seed=0))
     B, H, Wd = a.batch or W["batch"], W["h"], W["w"]
     ids = torch.randint(0, len(st), (a.launches, B), device="cuda")
     prec = a.precision or ("bf16" if a.config == "c3" else "fp32")
