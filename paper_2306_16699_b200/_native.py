@@ -5,11 +5,14 @@ import fails loudly (build it with ``python -m paper_2306_16699_b200.build``).""
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 from .errors import raise_for_status
 
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / "librinr_b200.so"
+# RINR_LIB_PATH selects another build of the same ABI (tools/checked_build.sh's
+# bounds-asserting library); the default is the in-tree product build
+LIB_PATH = Path(os.environ.get("RINR_LIB_PATH") or Path(__file__).resolve().parent / "_lib" / "librinr_b200.so")
 
 # enums (include/rinr_b200.h)
 OUT_F32, OUT_BF16, OUT_U8 = 0, 1, 2

@@ -227,11 +227,12 @@ int rinr_launch_dequantize(const StoreView& sv, const int64_t* d_ids, int64_t n,
 
 namespace {
 
-DecodeArgs make_args(const rinr_decode_params_t* p) {
+DecodeArgs make_args(const rinr_decode_params_t* p, int64_t n) {
   DecodeArgs a{};
   a.out_h = p->out_h;
   a.out_w = p->out_w;
   a.hw = p->out_h * p->out_w;
+  a.out_elems = n * 3 * int64_t(a.hw);
   a.inv_wm1 = p->out_w > 1 ? 1.0 / double(p->out_w - 1) : 0.0;
   a.inv_hm1 = p->out_h > 1 ? 1.0 / double(p->out_h - 1) : 0.0;
   a.dtype = p->out_dtype;
@@ -453,7 +454,7 @@ int rinr_launch_decode(const StoreView& sv, const HostArch* ua, const int64_t* d
                        void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   if (d_status && cudaMemsetAsync(d_status, 0, sizeof(int32_t), st) != cudaSuccess) return launch_fail("status reset");
-  const DecodeArgs a = make_args(p);
+  const DecodeArgs a = make_args(p, n);
   if (a.dtype == RINR_OUT_U8 && !a.identity)
     return set_error(RINR_ERR_INVALID_INPUT, "u8 output takes no mean/std normalisation");
   const bool acc = p->sin_mode == RINR_SIN_ACCURATE;

@@ -10,10 +10,41 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdio>
 
 #include "rinr_internal.h"
 
 namespace rinr {
+
+// Checked builds (-DRINR_CHECKED, tools/checked_build.sh): bounds of every
+// shared-memory access made through the helpers below, of record reads and of
+// output stores are asserted on the device (compute-sanitizer is not
+// available on the GPU pool).  Product builds compile the checks away.
+#ifdef RINR_CHECKED
+#define RINR_DCHECK(c)                                                              \
+  do {                                                                              \
+    if (!(c)) {                                                                     \
+      printf("RINR_DCHECK failed %s:%d block %d thread %d: %s\n", __FILE__, __LINE__, \
+             int(blockIdx.x), int(threadIdx.x), #c);                                \
+      __trap();                                                                     \
+    }                                                                               \
+  } while (0)
+#else
+#define RINR_DCHECK(c) \
+  do {                 \
+  } while (0)
+#endif
+
+// [p, p + bytes) lies inside this CTA's shared memory window: past the
+// reserved system region and below the end of the CTA's allocation
+// (%aggr_smem_size counts the reserved region too)
+__device__ __forceinline__ bool in_smem(const void* p, uint32_t bytes) {
+  uint32_t aggr, rsv_end;
+  asm("mov.u32 %0, %%aggr_smem_size;" : "=r"(aggr));
+  asm("mov.u32 %0, %%reserved_smem_offset_end;" : "=r"(rsv_end));
+  const uint64_t off = __cvta_generic_to_shared(p);
+  return __isShared(p) && off >= rsv_end && off + bytes <= aggr;
+}
 
 // ---------------------------------------------------------------------------
 // Byte access into a 16-B aligned shared-memory copy of a record.  Fields in
@@ -23,6 +54,7 @@ namespace rinr {
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t ld_u32u(const uint8_t* base, uint32_t off) {
   const uint32_t* w = reinterpret_cast<const uint32_t*>(base + (off & ~3u));
+  RINR_DCHECK(in_smem(w, 8));
   uint32_t lo = w[0], hi = w[1];
   return __funnelshift_r(lo, hi, (off & 3u) * 8u);
 }
@@ -202,6 +234,7 @@ __device__ __forceinline__ float value_at(const uint8_t* rec, const ValueRecipe&
   const uint32_t bit = uint32_t(j) & 31u;
   const bool kept = (wd >> bit) & 1u;
   const uint32_t vi = R.sparse ? pre + __popc(wd & ((1u << bit) - 1u)) : uint32_t(j);
+  RINR_DCHECK(in_smem(rec + R.vals_off + vi * uint32_t(R.esize), 1));
   if constexpr (INT) {
     const int code = int(rec[R.vals_off + vi]);
     return kept ? float(code - R.zp) : 0.0f;
@@ -248,6 +281,7 @@ __device__ __forceinline__ float grid_coord(int i, int n, double inv) {
 
 struct DecodeArgs {
   int out_h, out_w, hw;
+  int64_t out_elems;      // n * 3 * hw: bound of every output index (checked builds)
   double inv_wm1, inv_hm1;
   int dtype, layout, aug;
   int identity;           // mean 0 / std 1: skip the normalise arithmetic
@@ -300,6 +334,7 @@ __device__ __forceinline__ void store_value(const DecodeArgs& a, void* __restric
                                             float v) {
   const int64_t idx = a.layout == RINR_LAYOUT_NCHW ? (img * 3 + ch) * int64_t(a.hw) + p
                                                    : (img * int64_t(a.hw) + p) * 3 + ch;
+  RINR_DCHECK(idx >= 0 && idx < a.out_elems && p >= 0 && p < a.hw && ch >= 0 && ch < 3);
   if (a.dtype == RINR_OUT_F32) {
     static_cast<float*>(out)[idx] = v;
   } else if (a.dtype == RINR_OUT_BF16) {

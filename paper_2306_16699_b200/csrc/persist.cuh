@@ -23,6 +23,7 @@
 namespace rinr {
 
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
+  RINR_DCHECK(in_smem(smem_dst, 16));
   const uint32_t d = static_cast<uint32_t>(__cvta_generic_to_shared(smem_dst));
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gmem_src) : "memory");
 }
@@ -442,16 +443,21 @@ __device__ __forceinline__ void decode_group(const NetView<HID, NL>& net, const 
   for (int bk = 0; bk < NB; ++bk)
 #pragma unroll
     for (int e = 0; e < 4; ++e)
-      if (2 * tq + (e & 1) < 3) stage[(2 * tq + (e & 1)) * GPX + 16 * bk + g + 8 * (e >> 1)] = ov[bk][e];
+      if (2 * tq + (e & 1) < 3) {
+        RINR_DCHECK(in_smem(stage + (2 * tq + (e & 1)) * GPX + 16 * bk + g + 8 * (e >> 1), 4));
+        stage[(2 * tq + (e & 1)) * GPX + 16 * bk + g + 8 * (e >> 1)] = ov[bk][e];
+      }
   __syncwarp();
   // ---- coalesced stores -------------------------------------------------------------
   if constexpr (M::STORE == 1) {
     if (SL.active) {
+      RINR_DCHECK(gofs >= 0 && gofs + 4 <= a.out_elems);
       const float4 v = *reinterpret_cast<const float4*>(stage + SL.soff[0]);
       *reinterpret_cast<float4*>(static_cast<float*>(out) + gofs) = v;
     }
   } else if constexpr (M::STORE == 2) {
     if (SL.active) {
+      RINR_DCHECK(gofs >= 0 && gofs + 8 <= a.out_elems);
       const float4 u = *reinterpret_cast<const float4*>(stage + SL.soff[0]);
       const float4 w = *reinterpret_cast<const float4*>(stage + SL.soff[0] + 4);
       uint4 pk;
@@ -462,6 +468,8 @@ __device__ __forceinline__ void decode_group(const NetView<HID, NL>& net, const 
       *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(out) + gofs) = pk;
     }
   } else if constexpr (M::STORE == 3) {
+    if (SL.active)
+      RINR_DCHECK(gofs >= 0 && gofs + 4 <= a.out_elems);
     if (SL.active)
       *reinterpret_cast<float4*>(static_cast<float*>(out) + gofs) =
           make_float4(stage[SL.soff[0]], stage[SL.soff[1]], stage[SL.soff[2]], stage[SL.soff[3]]);

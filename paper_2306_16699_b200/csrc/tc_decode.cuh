@@ -405,6 +405,7 @@ __global__ void __launch_bounds__(4 * T * 32, 1)
       const uint32_t tahi = tacc + C::ahi_col(X3), talo = tacc + C::alo_col();
       const bool issuer = q == 0 && lane == 0;
       const uint32_t dslot = tmem_base + uint32_t(s * SLOT);
+      RINR_DCHECK((s + 1) * SLOT <= lay.tmem_cols);
       const float invW = 1.0f / float(a.out_w);
       for (int r = 0; r < rounds; ++r) {
         const int t = ts + r * T + s;
@@ -507,6 +508,7 @@ __global__ void __launch_bounds__(4 * T * 32, 1)
         // consecutive pixels x 3 channels go through a shared-memory stage
         // (the free phase-1 scratch) and out as 16-byte vector stores
         float* sw = reinterpret_cast<float*>(smem) + warp * 96;  // [ch][32 px]
+        RINR_DCHECK(in_smem(sw, 96 * 4) && warp * 96 * 4 + 384 <= lay.region0);
 #pragma unroll
         for (int ch = 0; ch < 3; ++ch) {
           float vv = __saturatef(o[ch] + net.biasO[ch]);
@@ -530,12 +532,14 @@ __global__ void __launch_bounds__(4 * T * 32, 1)
               pk.y = bf2_bits(__floats2bfloat162_rn(u.z, u.w));
               pk.z = bf2_bits(__floats2bfloat162_rn(v.x, v.y));
               pk.w = bf2_bits(__floats2bfloat162_rn(v.z, v.w));
+              RINR_DCHECK((img * 3 + ch) * int64_t(a.hw) + p0 + part * 8 + 8 <= a.out_elems);
               *reinterpret_cast<uint4*>(static_cast<__nv_bfloat16*>(out) + (img * 3 + ch) * int64_t(a.hw) + p0 +
                                         part * 8) = pk;
             }
           } else if (a.layout == RINR_LAYOUT_NCHW) {  // f32
             if (lane < 24) {
               const int ch = lane >> 3, part = lane & 7;
+              RINR_DCHECK((img * 3 + ch) * int64_t(a.hw) + p0 + part * 4 + 4 <= a.out_elems);
               *reinterpret_cast<float4*>(static_cast<float*>(out) + (img * 3 + ch) * int64_t(a.hw) + p0 + part * 4) =
                   *reinterpret_cast<const float4*>(sw + ch * 32 + part * 4);
             }
@@ -547,6 +551,7 @@ __global__ void __launch_bounds__(4 * T * 32, 1)
                 const int e = 4 * lane + k, px = e / 3, ch = e - 3 * px;
                 v4[k] = sw[ch * 32 + px];
               }
+              RINR_DCHECK((img * a.hw + p0) * 3 + 4 * lane + 4 <= a.out_elems);
               *reinterpret_cast<float4*>(static_cast<float*>(out) + (img * a.hw + p0) * 3 + 4 * lane) =
                   make_float4(v4[0], v4[1], v4[2], v4[3]);
             }
