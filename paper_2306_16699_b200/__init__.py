@@ -32,4 +32,7 @@ def __getattr__(name):
     if name in ("decode", "decode_batch", "install"):
         from . import decoder
         return getattr(decoder, name)
+    if name in ("read", "ArchiveReader", "materialize", "parse_record", "RawRecord", "RawLayer"):
+        from . import reader
+        return getattr(reader, name)
     raise AttributeError(name)

@@ -16,7 +16,7 @@ import torch
 from . import compressor
 from .archive import serialize_batch
 from .compressor import ModelBatch
-from .errors import BatchItemError, InvalidInputError
+from .errors import BatchItemError, InvalidInputError, RinrError
 from .image import ImageBuffer
 from .net import validate_model
 from .store import Store
@@ -104,22 +104,69 @@ def decode_batch(models, out_h: int | None = None, out_w: int | None = None, par
     return _decode_all(list(models), out_h, out_w, precision)
 
 
+def _translating(fn, err_mod):
+    """Wrap a drop-in so that the exceptions it raises are the rinr package's
+    own classes (same names and arguments; errors.py:8-50), as callers of the
+    reference catch them."""
+    import functools  # noqa: PLC0415
+
+    def translate(e):
+        cls = getattr(err_mod, type(e).__name__, None) if err_mod is not None else None
+        if cls is None:
+            return e
+        if type(e).__name__ == "BatchItemError":
+            return cls(e.index, translate(e.cause))
+        if type(e).__name__ == "IntegrityError":
+            return cls(str(e), record=getattr(e, "record", None))
+        if type(e).__name__ == "TrainingError":
+            return cls(str(e), step=getattr(e, "step", -1))
+        return cls(str(e))
+
+    @functools.wraps(fn)
+    def wrapped(*args, **kwargs):
+        try:
+            return fn(*args, **kwargs)
+        except RinrError as e:
+            raise translate(e) from e
+
+    return wrapped
+
+
 def install(rinr_module=None) -> None:
-    """Rebind ``rinr.decode``/``rinr.decode_batch`` (and the decoder
-    module's) and ``rinr.bench.bench`` to the GPU versions; results use
-    rinr's own ImageBuffer."""
+    """Rebind the reference package's decode path to the GPU versions:
+    ``rinr.decode`` / ``rinr.decode_batch`` (and the decoder module's),
+    ``rinr.read`` / ``rinr.archive.read`` / ``materialize`` /
+    ``ArchiveReader`` (reader.py) and ``rinr.bench.bench``.  Results are built
+    from rinr's own classes (ImageBuffer, InrModel, ...) and errors are raised
+    as rinr's exception classes."""
     global _image_cls
     if rinr_module is None:
         import rinr as rinr_module  # noqa: PLC0415
     import importlib  # noqa: PLC0415
-    dec_mod = importlib.import_module(rinr_module.__name__ + ".decoder")
-    img_mod = importlib.import_module(rinr_module.__name__ + ".image")
+
+    def sub(name):
+        try:
+            return importlib.import_module(rinr_module.__name__ + "." + name)
+        except ImportError:
+            return getattr(rinr_module, name, None)
+
+    dec_mod, img_mod, err_mod = sub("decoder"), sub("image"), sub("errors")
     _image_cls = img_mod.ImageBuffer
     for mod in (rinr_module, dec_mod):
-        mod.decode = decode
-        mod.decode_batch = decode_batch
-    try:  # rinr.bench.bench -> the GPU harness (same BenchReport fields)
+        mod.decode = _translating(decode, err_mod)
+        mod.decode_batch = _translating(decode_batch, err_mod)
+    arch_mod, net_mod, comp_mod = sub("archive"), sub("net"), sub("compressor")
+    if arch_mod is not None:  # reader drop-ins
+        from . import reader  # noqa: PLC0415
+        for key, mod in (("InrModel", net_mod), ("LayerWeights", net_mod), ("Architecture", net_mod),
+                         ("QuantInfo", comp_mod), ("LayerQuant", comp_mod), ("ArchiveRecord", arch_mod),
+                         ("DatasetArchive", arch_mod)):
+            if mod is not None and hasattr(mod, key):
+                reader.TYPES[key] = getattr(mod, key)
+        for mod in (rinr_module, arch_mod):
+            mod.read = _translating(reader.read, err_mod)
+        arch_mod.materialize = _translating(reader.materialize, err_mod)
+    bench_mod = sub("bench")
+    if bench_mod is not None:  # rinr.bench.bench -> the GPU harness (same BenchReport fields)
         from .harness import bench as gpu_bench  # noqa: PLC0415
-        importlib.import_module(rinr_module.__name__ + ".bench").bench = gpu_bench
-    except ImportError:
-        pass
+        bench_mod.bench = gpu_bench

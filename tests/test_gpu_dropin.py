@@ -44,8 +44,9 @@ def test_install_rebinds_fake_package():
     pkg = _fake_rinr()
     try:
         decoder.install(pkg)
-        assert pkg.decode_batch is decoder.decode_batch and pkg.decoder.decode_batch is decoder.decode_batch
-        assert pkg.decode is decoder.decode and pkg.decoder.decode is decoder.decode
+        assert pkg.decode_batch.__wrapped__ is decoder.decode_batch
+        assert pkg.decoder.decode_batch.__wrapped__ is decoder.decode_batch
+        assert pkg.decode.__wrapped__ is decoder.decode and pkg.decoder.decode.__wrapped__ is decoder.decode
         assert pkg.bench.bench is harness.bench
         models = [synth.config2(6, 0).model(i) for i in range(6)]
         imgs = pkg.decode_batch(models, 32, 32)
