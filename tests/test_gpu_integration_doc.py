@@ -54,3 +54,20 @@ def test_decode_stub_runs(monkeypatch, tmp_path):
     env["lib"].rinr_store_destroy(env["store"])
     rt.cudaFree(env["d_ids"])
     rt.cudaFree(env["d_out"])
+
+
+def test_writer_stub_runs(monkeypatch):
+    """Section 2b's writer stub produces the reference writer's bytes."""
+    import torch
+    from paper_2306_16699_b200 import synth, transforms as T
+    from paper_2306_16699_b200.archive import serialize_batch
+    monkeypatch.chdir(ROOT)
+    mb = synth.config1(16)
+    mb.source_h, mb.source_w = 32, 32
+    dm = T.DeviceModels.from_batch(mb)
+    code = [b for b in _blocks() if "rinr_serialize_size.argtypes" in b]
+    assert len(code) == 1
+    env = {"w": dm.w, "mask": dm.mask, "b": dm.b}
+    exec(compile(code[0], "INTEGRATION.md", "exec"), env)
+    torch.cuda.synchronize()
+    assert env["data"] == serialize_batch(dm.to_batch(), [f"img{i:08d}" for i in range(16)])

@@ -1,23 +1,27 @@
 #!/bin/bash
-# Round evidence refresh (run on the GPU box via gpurun); outputs under gpurun_out/.
-#   bash tools/profile_round.sh [c2|c3|all]
+# Round evidence refresh on the GPU box (gpurun); outputs under gpurun_out/r02/.
+#   bash tools/profile_round.sh
+# 1. the GPU suite; 2. the driver's bench commands (ours + reference arm);
+# 3. c4 / c5 training benches; 4. ncu launch list of the default bench;
+# 5. one `ncu --set full` capture per decode kernel of the metric (c2 fp32,
+#    c1 fp32, c3 fp32, c3 bf16), each after the same command ran clean.
 set -o pipefail
-what=${1:-all}
-o=gpurun_out
+o=gpurun_out/r02
 mkdir -p $o
-timeout 900 python -m pytest tests -m gpu -q > $o/pytest_gpu.log 2>&1; tail -1 $o/pytest_gpu.log
-if [ "$what" != "c3" ]; then
-  python bench.py > $o/bench_c2.json 2> $o/bench_c2.err || tail -5 $o/bench_c2.err
-  python bench.py --precision bf16 --no-cpu --no-e2e > $o/bench_c2_bf16.json 2>> $o/bench_c2.err
-  ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file $o/launches_c2.csv \
-    python bench.py --steps 20 --warmup 3 --no-cpu --no-e2e > $o/ncu_launch.log 2>&1
-  ncu --set full --clock-control none --import-source on -k regex:decode_persist -s 10 -c 1 -o $o/full_c2 -f \
-    python bench.py --steps 20 --warmup 3 --no-cpu --no-e2e > $o/ncu_full_c2.log 2>&1
-fi
-if [ "$what" != "c2" ]; then
-  python bench.py --config c3 --steps 20 --warmup 3 > $o/bench_c3.json 2> $o/bench_c3.err || tail -5 $o/bench_c3.err
-  python bench.py --config c3 --steps 20 --warmup 3 --precision fp32 --no-cpu --no-e2e > $o/bench_c3_fp32.json 2>> $o/bench_c3.err
-  ncu --set full --clock-control none --import-source on -k regex:decode_tc -s 5 -c 1 -o $o/full_c3 -f \
-    python bench.py --config c3 --steps 5 --warmup 3 --no-cpu --no-e2e --store-records 512 > $o/ncu_full_c3.log 2>&1
-fi
-for f in $o/bench_*.json; do echo "$f: $(python -c "import json,sys; d=json.loads(open('$f').read().strip().splitlines()[-1]); print(round(d['value']), d['unit'], 'frac', round(d['roofline']['frac'],3), 'ms', round(d['ms_per_step'],5), 'e2e', (d.get('e2e') or {}).get('value'))")"; done
+timeout 1200 python -m pytest tests -m gpu -q > $o/pytest_gpu.log 2>&1; tail -1 $o/pytest_gpu.log
+python bench.py --steps 20 --warmup 5 > $o/bench.json 2> $o/bench.err || tail -5 $o/bench.err
+python bench.py --impl reference --steps 20 --warmup 5 > $o/bench_ref.json 2> $o/bench_ref.err || tail -5 $o/bench_ref.err
+python bench.py --config c4 --steps 20 --warmup 5 > $o/bench_c4.json 2> $o/bench_c4.err || tail -5 $o/bench_c4.err
+python bench.py --config c5 --steps 20 --warmup 5 > $o/bench_c5.json 2> $o/bench_c5.err || tail -5 $o/bench_c5.err
+ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file $o/launches_bench.csv \
+  python bench.py --steps 20 --warmup 5 --no-cpu --no-e2e > $o/ncu_launch.log 2>&1
+for spec in "c2 fp32 decode_persist 1024" "c1 fp32 decode_persist 256" "c3 fp32 decode_tc 256" "c3 bf16 decode_tc 256"; do
+  set -- $spec
+  cmd="python tools/ncu_decode.py --config $1 --precision $2 --launches 6 --records 65536"
+  [ "$1" = "c3" ] && cmd="python tools/ncu_decode.py --config $1 --precision $2 --launches 4 --records 16384"
+  $cmd > $o/plain_$1_$2.log 2>&1 && \
+  ncu --set full --clock-control none --import-source on -k regex:$3 -s 3 -c 1 -o $o/full_$1_$2 -f $cmd \
+    > $o/ncu_full_$1_$2.log 2>&1
+  tail -1 $o/ncu_full_$1_$2.log
+done
+ls $o
