@@ -145,8 +145,11 @@ def _assemble(fields: list, n: int) -> tuple:
         width = f.mat.shape[1]
         if width == 0:
             continue
-        sel = np.arange(width)[None, :] < f.lens[:, None]
         dest = field_start[:, fi][:, None] + np.arange(width)[None, :]
+        if bool((f.lens == width).all()):  # every record writes the full row: no compaction
+            out[dest] = f.mat
+            continue
+        sel = np.arange(width)[None, :] < f.lens[:, None]
         out[dest[sel]] = f.mat[sel]
     return out, starts, body
 
