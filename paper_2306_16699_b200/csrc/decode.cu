@@ -211,6 +211,17 @@ static size_t prefix_bytes(const StoreView& sv) {
 
 using namespace rinr;
 
+#ifdef RINR_DEV_KNOBS
+// Development builds: the decode_persist timeline ([4][512][8] u64 ns) and
+// dequant task durations ([512][16][2] u64).
+extern "C" RINR_API int rinr_dev_times(unsigned long long* host) {
+  return cudaMemcpyFromSymbol(host, g_dev_t, sizeof(g_dev_t)) == cudaSuccess ? RINR_OK : RINR_ERR_CUDA;
+}
+extern "C" RINR_API int rinr_dev_task_times(unsigned long long* host) {
+  return cudaMemcpyFromSymbol(host, g_dev_task, sizeof(g_dev_task)) == cudaSuccess ? RINR_OK : RINR_ERR_CUDA;
+}
+#endif
+
 int rinr_launch_dequantize(const StoreView& sv, const int64_t* d_ids, int64_t n, float* d_out, int64_t out_stride,
                            int32_t* d_status, void* stream) {
   cudaStream_t st = static_cast<cudaStream_t>(stream);
@@ -300,7 +311,11 @@ int launch_persist(const StoreView& sv, const int64_t* ids, int64_t n, const Dec
 #else
   constexpr int dbg = 0;
 #endif
-  const int overlap = ((flags & RINR_FLAG_OVERLAP_PROLOGUE) ? 1 : 0) | (dbg << 1);
+  int overlap = ((flags & RINR_FLAG_OVERLAP_PROLOGUE) ? 1 : 0) | (dbg << 1);
+#ifdef RINR_DEV_KNOBS
+  static std::atomic<int> dev_slot{0};
+  overlap |= (dev_slot++ & 3) << 4;  // timeline slot of this launch (dev_stamp)
+#endif
   if (cudaLaunchKernelEx(&cfg, kern, sv, ids, n, a, aug, out, status, omega, lay, overlap) != cudaSuccess)
     return launch_fail("decode_persist launch");
 

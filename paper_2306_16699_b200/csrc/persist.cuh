@@ -33,6 +33,23 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+#ifdef RINR_DEV_KNOBS
+// Development timeline (RINR_DEV_KNOBS builds only, tools/dev_timeline.py):
+// %globaltimer of each CTA's thread 0 at the phase boundaries of the last 4
+// launches, and clock64 durations of each warp's first dequant task.
+__device__ unsigned long long g_dev_t[4][512][8];
+__device__ unsigned long long g_dev_task[512][16][2];
+__device__ __forceinline__ void dev_stamp(int overlap, int stage) {
+  if (threadIdx.x == 0 && blockIdx.x < 512) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    g_dev_t[(overlap >> 4) & 3][blockIdx.x][stage] = t;
+  }
+}
+#else
+__device__ __forceinline__ void dev_stamp(int, int) {}
+#endif
+
 struct PersistLayout {
   int maxi;        // images per chunk
   int net_words;   // per image
@@ -608,6 +625,7 @@ __global__ void __launch_bounds__(NW * 32, (NW < 16 ? 16 / NW : 1))
   int64_t* metaid = reinterpret_cast<int64_t*>(pfx + lay.maxi * lay.pfx_words);  // [maxi]
   float* stagebase = reinterpret_cast<float*>(metaid + ((lay.maxi + 1) & ~1));
 
+  dev_stamp(overlap, 0);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nblk = (a.hw + 15) / 16;
   const int gpi = (nblk + NB - 1) / NB;  // groups per image
@@ -639,6 +657,7 @@ __global__ void __launch_bounds__(NW * 32, (NW < 16 ? 16 / NW : 1))
     for (int i = warp; i < ni; i += NW) {
       const int64_t id = ids[cimg + i];
       const bool ok = id >= 0 && id < sv.n;
+      if (c0 == 0 && i == 0 && ok) dev_stamp(overlap, 7);
       if (lane == 0) {
         if (!ok) flag_bad_id(status, n, cimg + i);
         metaid[i] = ok ? id : -1;
@@ -652,6 +671,7 @@ __global__ void __launch_bounds__(NW * 32, (NW < 16 ? 16 / NW : 1))
       for (uint32_t k = lane; k < bytes / 16; k += 32) cp_async16(dst + 16 * k, src + 16 * k);
     }
     cp_async_commit();
+    if (c0 == 0) dev_stamp(overlap, 1);
     if constexpr (!FRAG_TASKS)
       for (int i = tid; i < ni * lay.net_words / 4; i += NT) reinterpret_cast<uint4*>(nets)[i] = make_uint4(0, 0, 0, 0);
     if (!shared_tab)
@@ -661,6 +681,7 @@ __global__ void __launch_bounds__(NW * 32, (NW < 16 ? 16 / NW : 1))
       }
     cp_async_wait_all();
     __syncthreads();
+    if (c0 == 0) dev_stamp(overlap, 2);
     // Dequantise straight into MMA fragments: task (image i, part h) with
     // h = 0 -> layer 0 + output layer, h = 1..NH -> hidden layer h.  Every
     // lane writes exactly the fragment words it owns (padding included), so
@@ -670,8 +691,18 @@ __global__ void __launch_bounds__(NW * 32, (NW < 16 ? 16 / NW : 1))
       for (int task = (overlap & 4) ? ni * TPI : warp; task < ni * TPI; task += NW) {
         const int i = task / TPI, h = task - i * TPI;
         if (metaid[i] < 0) continue;
+#ifdef RINR_DEV_KNOBS
+        const unsigned long long t_a = clock64();
+#endif
         frag_task<HID, NL, M::INTB>(sv, recs + size_t(i) * lay.rec_bytes, h, Net(nets + i * lay.net_words), omega,
                                     lane);
+#ifdef RINR_DEV_KNOBS
+        __syncwarp();
+        if (lane == 0 && blockIdx.x < 512 && warp < 16 && task == warp) {
+          g_dev_task[blockIdx.x][warp][0] = t_a;
+          g_dev_task[blockIdx.x][warp][1] = clock64() - t_a + 1000000ull * h;
+        }
+#endif
       }
     }
     // Dequantise: one warp per (image, layer) task — the layer header is parsed
@@ -726,8 +757,10 @@ __global__ void __launch_bounds__(NW * 32, (NW < 16 ? 16 / NW : 1))
     __syncthreads();
     // -------------------------------- phase 2 --------------------------------
     if (c0 == 0) {
+      dev_stamp(overlap, 3);
       if (overlap & 1) pdl_wait();  // outputs may still be read/written by the preceding grid
       pdl_trigger();            // every CTA is resident: the next launch may start its prologue
+      dev_stamp(overlap, 4);
     }
     const int64_t cbase = cimg * gpi;
     const int gs = int((G0 > cbase ? G0 : cbase) - cbase);
@@ -735,8 +768,10 @@ __global__ void __launch_bounds__(NW * 32, (NW < 16 ? 16 / NW : 1))
     if (!(overlap & 2))
       phase2_loop<HID, NL, X3, ACCURATE, NW, NB, M>(nets, tabs, lay, shared_tab, a, out, cimg, gs, ge, gpi, invW,
                                                     stage, warp, lane);
+    if (c0 == 0) dev_stamp(overlap, 5);
     __syncthreads();
   }
+  dev_stamp(overlap, 6);
 }
 
 }  // namespace rinr

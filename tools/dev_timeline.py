@@ -1,0 +1,42 @@
+"""Per-CTA phase timeline of decode_persist (library built with
+RINR_EXTRA_NVCC_FLAGS=-DRINR_DEV_KNOBS; tools/dev_timeline.sh)."""
+import ctypes as C
+import sys
+
+sys.path.insert(0, ".")
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2306_16699_b200 import Store, _native, synth  # noqa: E402
+
+cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
+B = 1024 if cfg == "c2" else 256
+st = Store(synth.gpu_store_bytes(cfg, 65536, seed=3))
+ids = torch.randint(0, len(st), (16, B), device="cuda")
+p = st.decode_params(32, 32, precision="fp32", overlap_prologue=True)
+out = torch.empty((B, 3, 32, 32), device="cuda")
+for k in range(12):  # back to back on one stream (PDL chain), last 4 recorded
+    st.decode(ids[k], out=out, params=p, check=False)
+torch.cuda.synchronize()
+t = np.zeros((4, 512, 8), np.uint64)
+assert _native.lib().rinr_dev_times(t.ctypes.data_as(C.c_void_p)) == 0
+grid = 148
+t = t[:, :grid, :].astype(np.int64)
+base = t[:, :, 0].min()
+names = ["entry", "ids+cp.async issued", "records in smem", "dequant done", "pdl_wait done", "phase2 done", "exit"]
+for s in range(4):
+    tt = t[s] - base
+    print(f"launch slot {s}: entry {tt[:, 0].min() / 1e3:.2f}..{tt[:, 0].max() / 1e3:.2f} us, "
+          f"exit {tt[:, 6].min() / 1e3:.2f}..{tt[:, 6].max() / 1e3:.2f} us")
+    d7 = (t[s][:, 7] - t[s][:, 0]) / 1e3
+    print(f"   entry -> first id loaded: median {np.median(d7):.2f} us  max {d7.max():.2f}")
+    for k in range(1, 7):
+        d = (t[s][:, k] - t[s][:, k - 1]) / 1e3
+        print(f"   {names[k - 1]:>22s} -> {names[k]:<22s} median {np.median(d):6.2f} us  max {d.max():6.2f}")
+tk = np.zeros((512, 16, 2), np.uint64)
+assert _native.lib().rinr_dev_task_times(tk.ctypes.data_as(C.c_void_p)) == 0
+d = tk[:grid, :, 1].astype(np.int64)
+for h in (0, 1):
+    sel = d[(d >= h * 1000000) & (d < (h + 1) * 1000000)] - h * 1000000
+    if sel.size:
+        print(f"task h={h}: {sel.size} samples, median {np.median(sel):.0f} cycles, max {sel.max()}")
