@@ -5,12 +5,16 @@
  *
  * Models use the transform layout of rinr_b200_transforms.h: d_w [n][P] f32
  * (matrices concatenated, row-major (out, in)), d_b [n][sum dims[1..]] f32,
- * d_mask [n][P] u8.  Supported architectures: (2, H, H, 3) with 8 <= H <= 16 (all widths built)
- * (the CIFAR net of PAPER.md:441 is H = 15); others return
- * RINR_ERR_UNSUPPORTED.
+ * d_mask [n][P] u8.  Architectures: (2, H, H, 3) with 8 <= H <= 16 run the
+ * fused narrow kernel (the CIFAR net of PAPER.md:441 is H = 15); any other
+ * (2, d1, ..., 3) with widths <= 64 and <= 16 weight matrices (the 10-layer
+ * 102flowers / Mini-ImageNet nets) runs the general kernels
+ * (fit_general.cu: per Adam step one forward/backward launch over 32-pixel
+ * tiles with several CTAs per image and one update launch).
  *
- * One CTA fits one image.  All `steps` Adam steps of a round run inside one
- * launch, with weights, moments and masks in shared memory.  The arithmetic
+ * Narrow kernel: one CTA fits one image and all `steps` Adam steps of a
+ * round run inside one launch, with weights, moments and masks in shared
+ * memory.  The arithmetic
  * follows the reference's fp32 algorithm:
  *   * RINR_SIN_ACCURATE: forward / backward per pixel in fp32 FFMA with
  *     accurate sinf, gradient sums in 3xTF32 (fp32-accurate);

@@ -21,7 +21,7 @@ CSRC = PKG / "csrc"
 # tools/checked_build.sh goes to _lib_checked/)
 LIB_DIR = Path(os.environ["RINR_LIB_DIR"]) if os.environ.get("RINR_LIB_DIR") else PKG / "_lib"
 LIB = LIB_DIR / "librinr_b200.so"
-SOURCES = [CSRC / "store.cpp", CSRC / "decode.cu", CSRC / "diag.cu", CSRC / "transforms.cu", CSRC / "fit.cu", CSRC / "writer.cu"]
+SOURCES = [CSRC / "store.cpp", CSRC / "decode.cu", CSRC / "diag.cu", CSRC / "transforms.cu", CSRC / "fit.cu", CSRC / "fit_general.cu", CSRC / "writer.cu"]
 HEADERS = [ROOT / "include" / "rinr_b200.h", ROOT / "include" / "rinr_b200_diag.h", ROOT / "include" / "rinr_b200_transforms.h", ROOT / "include" / "rinr_b200_encoder.h", ROOT / "include" / "rinr_b200_writer.h", CSRC / "rinr_internal.h", CSRC / "device_common.cuh", CSRC / "mma_chain.cuh", CSRC / "persist.cuh", CSRC / "tc_decode.cuh"]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -1028,12 +1028,21 @@ int launch_render(int64_t n, const float* w, const float* b, int h, int wd, doub
 
 using namespace rinr;
 
+// General architectures (fit_general.cu)
+int rinr_fit_general(const int32_t* dims, int nl, int64_t n, float* d_w, float* d_b, const uint8_t* d_mask,
+                     const float* d_images, const rinr_fit_params_t* p, double* d_curve, int32_t* d_status,
+                     float* d_grad_w, float* d_grad_b, double* d_loss0, void* stream);
+int rinr_fit_render_general(const int32_t* dims, int nl, int64_t n, const float* d_w, const float* d_b, int32_t h,
+                            int32_t w, double omega, int32_t sin_mode, float* d_out, void* stream);
+
+static bool narrow_arch(const int32_t* dims, int nl) {
+  return dims && nl == 3 && dims[0] == 2 && dims[3] == 3 && dims[1] == dims[2] && dims[1] >= 8 && dims[1] <= 16;
+}
+
 extern "C" int rinr_fit(const int32_t* dims, int nl, int64_t n, float* d_w, float* d_b, const uint8_t* d_mask,
                         const float* d_images, const rinr_fit_params_t* p, double* d_curve, int32_t* d_status,
                         float* d_grad_w, float* d_grad_b, double* d_loss0, void* stream) {
   clear_error();
-  int H = 0;
-  if (int e = fit_arch(dims, nl, H)) return e;
   if (!p || n < 0) return set_error(RINR_ERR_INVALID_INPUT, "null params or negative n");
   if (p->h < 1 || p->w < 1 || p->steps < 0 || p->curve_cap < 1) return set_error(RINR_ERR_INVALID_INPUT, "bad fit params");
   if (n == 0) return RINR_OK;
@@ -1041,6 +1050,11 @@ extern "C" int rinr_fit(const int32_t* dims, int nl, int64_t n, float* d_w, floa
     return set_error(RINR_ERR_INVALID_INPUT, "null buffer");
   if ((d_grad_w == nullptr) != (d_grad_b == nullptr) || (d_grad_w && !d_loss0))
     return set_error(RINR_ERR_INVALID_INPUT, "grad outputs need d_grad_w, d_grad_b and d_loss0");
+  if (!narrow_arch(dims, nl))  // deep / wide nets: the general per-step kernels
+    return rinr_fit_general(dims, nl, n, d_w, d_b, d_mask, d_images, p, d_curve, d_status, d_grad_w, d_grad_b,
+                            d_loss0, stream);
+  int H = 0;
+  if (int e = fit_arch(dims, nl, H)) return e;
   FitArgs a{};
   a.n = n;
   a.w = d_w;
@@ -1078,11 +1092,12 @@ extern "C" int rinr_fit(const int32_t* dims, int nl, int64_t n, float* d_w, floa
 extern "C" int rinr_fit_render(const int32_t* dims, int nl, int64_t n, const float* d_w, const float* d_b, int32_t h,
                                int32_t w, double omega, int32_t sin_mode, float* d_out, void* stream) {
   clear_error();
-  int H = 0;
-  if (int e = fit_arch(dims, nl, H)) return e;
   if (n < 0 || h < 1 || w < 1) return set_error(RINR_ERR_INVALID_INPUT, "bad render size");
   if (n == 0) return RINR_OK;
   if (!d_w || !d_b || !d_out) return set_error(RINR_ERR_INVALID_INPUT, "null buffer");
+  if (!narrow_arch(dims, nl)) return rinr_fit_render_general(dims, nl, n, d_w, d_b, h, w, omega, sin_mode, d_out, stream);
+  int H = 0;
+  if (int e = fit_arch(dims, nl, H)) return e;
   cudaStream_t st = static_cast<cudaStream_t>(stream);
   const bool acc = sin_mode == RINR_SIN_ACCURATE;
   switch (H) {

@@ -300,6 +300,31 @@ def encoder_case():
     out["full/ratio"] = np.float64(rf.final_prune_ratio)
     out["derive_seed"] = np.array([encoder.derive_seed(s, i) for s in (0, 7, 2**40) for i in (0, 1, 999)],
                                   np.uint64)
+    # (4) wide / deep nets (the general GPU encoder): loss_and_grad of the
+    # Mini-ImageNet arch [2,40x9,3] (fresh and pruned) and 20 _train steps of
+    # a 4-layer 32-wide net, on 12x12 images
+    imgs12 = test_images(2, 12, 12, seed=23)
+    out["images12"] = imgs12
+    c12 = net.coordinate_grid(12, 12)
+    for k, seed in enumerate((41, 42)):
+        m = net.init(ARCH_C, seed)
+        if k == 1:
+            m = compressor.prune_l1(m, 0.3)
+            for l in m.layers:
+                l.b[:] = np.random.default_rng(seed).normal(0, 0.02, l.b.shape).astype(np.float32)
+        loss, grads = net.loss_and_grad(m, c12, imgs12[k].reshape(-1, 3))
+        out[f"wgrad{k}/w"] = np.concatenate([l.w.ravel() for l in m.layers])
+        out[f"wgrad{k}/b"] = np.concatenate([l.b.ravel() for l in m.layers])
+        out[f"wgrad{k}/mask"] = np.concatenate([x.ravel() for x in m.mask]).astype(np.uint8)
+        out[f"wgrad{k}/loss"] = np.float64(loss)
+        out[f"wgrad{k}/gw"] = np.concatenate([g.w.ravel() for g in grads])
+        out[f"wgrad{k}/gb"] = np.concatenate([g.b.ravel() for g in grads])
+    arch_d = net.Architecture((2, 32, 32, 32, 3))
+    m = net.init(arch_d, 44)
+    curve = []
+    encoder._train(m, c12, imgs12[1].reshape(-1, 3), 2e-4, 20, curve)
+    out["wtrain/curve"] = np.array(curve)
+    out["wtrain/w"] = np.concatenate([l.w.ravel() for l in m.layers])
     np.savez_compressed(OUT / "encoder.npz", **out)
 
 

@@ -164,3 +164,24 @@ def test_fitted_oracle(golden):
         np.testing.assert_array_equal(got.view(np.uint32), g[f"{name}/decode"].view(np.uint32))
         for i in range(len(models)):
             assert abs(O.psnr(got[i], g[f"{name}/source"][i]) - g[f"{name}/psnr"][i]) <= 1e-9
+
+
+def test_wide_training_oracle(golden):
+    """The oracle's loss_and_grad / train on the wide and deep nets the
+    general GPU encoder handles (reference fixtures: encoder.npz 'wgrad*',
+    'wtrain')."""
+    from transforms_common import split, split_bias
+    g = golden("encoder")
+    dims = (2, *[40] * 9, 3)
+    coords = O.coordinate_grid(12, 12)
+    for k in (0, 1):
+        ws = split(g[f"wgrad{k}/w"], dims)
+        bs = split_bias(g[f"wgrad{k}/b"], dims)
+        ms = split(g[f"wgrad{k}/mask"], dims, bool)
+        loss, gws, gbs = O.loss_and_grad(ws, bs, ms, 30.0, coords, g["images12"][k].reshape(-1, 3))
+        assert abs(loss - g[f"wgrad{k}/loss"]) <= 1e-12 * g[f"wgrad{k}/loss"]
+        np.testing.assert_allclose(np.concatenate([x.ravel() for x in gws]), g[f"wgrad{k}/gw"], rtol=1e-5, atol=1e-9)
+    d4 = (2, 32, 32, 32, 3)
+    ws, bs, ms = O.init_model(d4, 44)
+    curve = O.train(ws, bs, ms, 30.0, coords, g["images12"][1].reshape(-1, 3), 2e-4, 20)
+    np.testing.assert_allclose(curve, g["wtrain/curve"], rtol=1e-6)
