@@ -368,7 +368,7 @@ int garch_of(const int32_t* dims, int nl, GArch& A) {
     A.P += dims[l] * dims[l + 1];
     A.PB += dims[l + 1];
   }
-  if (gen_smem_floats(A) * 4 > 227 * 1024) return set_error(RINR_ERR_UNSUPPORTED, "GPU encoder: architecture too large");
+  if (gen_smem_floats(A) * 4 > 226 * 1024) return set_error(RINR_ERR_UNSUPPORTED, "GPU encoder: architecture too large");
   return RINR_OK;
 }
 
@@ -422,20 +422,17 @@ int rinr_fit_general(const int32_t* dims, int nl, int64_t n, float* d_w, float* 
     cudaGetLastError();
     return set_error(RINR_ERR_OOM, "GPU encoder workspace");
   }
-  float* grad = static_cast<float*>(ws);
+  double* loss = static_cast<double*>(ws);  // f64 first: 8-byte aligned whatever n * NP is
+  float* grad = reinterpret_cast<float*>(loss + n);
   float* mom = grad + n * NP;
   float* vel = mom + n * NP;
-  double* loss = reinterpret_cast<double*>(vel + n * NP);
-  int32_t* slots = reinterpret_cast<int32_t*>(loss + n);
+  int32_t* slots = reinterpret_cast<int32_t*>(vel + n * NP);
   if (cudaMemsetAsync(ws, 0, bytes, st) != cudaSuccess || cudaMemsetAsync(d_status, 0, size_t(n) * 4, st) != cudaSuccess)
     return set_error(RINR_ERR_CUDA, "GPU encoder workspace reset");
   const size_t smem = gen_smem_floats(A) * 4;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(gen_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)
-      return set_error(RINR_ERR_CUDA, "encoder smem attribute");
-    attr = true;
-  }
+  // (per call: the attribute is per device and cheap to set)
+  if (cudaFuncSetAttribute(gen_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess)
+    return set_error(RINR_ERR_CUDA, "encoder smem attribute");
   GStep s{};
   s.steps = p->steps;
   s.cap = p->curve_cap;
@@ -462,12 +459,8 @@ int rinr_fit_render_general(const int32_t* dims, int nl, int64_t n, const float*
   if (int e = garch_of(dims, nl, A)) return e;
   const GArgs g = make_gargs(A, n, nullptr, h, w, omega, sin_mode == RINR_SIN_ACCURATE);
   const size_t smem = (size_t(A.P + A.PB) + size_t(2) * A.maxw * kTile) * 4;
-  static bool attr = false;
-  if (!attr) {
-    if (cudaFuncSetAttribute(gen_render_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) != cudaSuccess)
-      return set_error(RINR_ERR_CUDA, "render smem attribute");
-    attr = true;
-  }
+  if (cudaFuncSetAttribute(gen_render_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess)
+    return set_error(RINR_ERR_CUDA, "render smem attribute");
   gen_render_kernel<<<dim3(unsigned(g.ctas_per_image), unsigned(n)), kGThreads, smem, static_cast<cudaStream_t>(stream)>>>(
       g, d_w, d_b, d_out);
   return cuda_err("GPU encoder render");

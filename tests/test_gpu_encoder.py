@@ -118,10 +118,15 @@ def test_encode_dataset_roundtrip(E):
 
 
 def test_unsupported(E):
+    """Widths above 64 (the general kernel's limit) are refused; (2, 20, 20, 3)
+    now runs on the general kernels."""
     from paper_2306_16699_b200 import UnsupportedError
-    dm = E.init_batch(E.Architecture((2, 20, 20, 3)), [0], 8, 8)
+    dm = E.init_batch(E.Architecture((2, 80, 3)), [0], 8, 8)
     with pytest.raises(UnsupportedError):
         E.train_batch(dm, torch.zeros((1, 8, 8, 3), device="cuda"), 1e-3, 2)
+    dm = E.init_batch(E.Architecture((2, 20, 20, 3)), [0], 8, 8)
+    curves, status = E.train_batch(dm, torch.full((1, 8, 8, 3), 0.5, device="cuda"), 1e-3, 4)
+    assert status[0] == 0 and np.isfinite(curves[0][:2]).all()
 
 
 @pytest.mark.parametrize("H", [8, 9, 12, 13, 14, 16])
