@@ -42,7 +42,9 @@ namespace {
 constexpr int kGMaxL = 16;   // weight matrices
 constexpr int kGMaxW = 64;   // widths
 constexpr int kTile = 32;    // pixels per tile
-constexpr int kGThreads = 128;
+constexpr int kGThreads = 256;
+constexpr int kGroups = kGThreads / 32;          // pixel-lane groups (warps)
+constexpr int kPerT = (kGMaxW + kGroups - 1) / kGroups;  // outputs per thread (register tile)
 
 struct GArch {
   int nl;
@@ -81,16 +83,57 @@ __host__ __device__ inline size_t gen_smem_floats(const GArch& A) {
   return size_t(2) * (A.P + A.PB) + size_t(A.nl - 1) * A.maxw * kTile + size_t(4) * A.maxw * kTile + 64;
 }
 
-// z_out[o][px] = sum_i W[o][i] in[i][px] + b[o] for one tile; 128 threads:
-// thread -> (px = t % 32, output group t / 32).
+// z_out[o][px] = sum_i W[o][i] in[i][px] + b[o] for one tile.  Thread ->
+// (px = t % 32, outputs o = t/32 + 8k): each input activation is loaded once
+// and reused for the thread's kPerT outputs (register tile).
 __device__ __forceinline__ void tile_linear(const float* W, const float* b, int fi, int fo, const float* in,
                                             float* out, int tid) {
-  const int px = tid & 31;
-  for (int o = tid >> 5; o < fo; o += kGThreads / 32) {
-    const float* wr = W + o * fi;
-    float z = 0.0f;
-    for (int i = 0; i < fi; ++i) z = fmaf(in[i * kTile + px], wr[i], z);
-    out[o * kTile + px] = __fadd_rn(z, b[o]);
+  const int px = tid & 31, og = tid >> 5;
+  float z[kPerT];
+#pragma unroll
+  for (int k = 0; k < kPerT; ++k) z[k] = 0.0f;
+  for (int i = 0; i < fi; ++i) {
+    const float a = in[i * kTile + px];
+#pragma unroll
+    for (int k = 0; k < kPerT; ++k) {
+      const int o = og + kGroups * k;
+      if (o < fo) z[k] = fmaf(a, W[o * fi + i], z[k]);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < kPerT; ++k) {
+    const int o = og + kGroups * k;
+    if (o < fo) out[o * kTile + px] = __fadd_rn(z[k], b[o]);
+  }
+}
+
+// gW[o][i] += sum_q delta[o][q] a[i][q] and gb[o] += sum_q delta[o][q] over
+// the tile, with 2 x 4 register tiles of (o, i) per thread.
+__device__ __forceinline__ void tile_grads(const float* dcur, const float* ain, int fi, int fo, float* gw, float* gb,
+                                           int tid) {
+  const int nib = (fi + 3) / 4, ntile = ((fo + 1) / 2) * nib;
+  for (int t = tid; t < ntile; t += kGThreads) {
+    const int o0 = 2 * (t / nib), i0 = 4 * (t - (t / nib) * nib);
+    float acc[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+    for (int q = 0; q < kTile; ++q) {
+      const float d0 = dcur[o0 * kTile + q], d1 = o0 + 1 < fo ? dcur[(o0 + 1) * kTile + q] : 0.0f;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        const float a = i0 + c < fi ? ain[(i0 + c) * kTile + q] : 0.0f;
+        acc[0][c] = fmaf(d0, a, acc[0][c]);
+        acc[1][c] = fmaf(d1, a, acc[1][c]);
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 2; ++r)
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        if (o0 + r < fo && i0 + c < fi) gw[(o0 + r) * fi + i0 + c] = __fadd_rn(gw[(o0 + r) * fi + i0 + c], acc[r][c]);
+  }
+  for (int o = tid; o < fo; o += kGThreads) {
+    float sacc = 0.0f;
+    for (int q = 0; q < kTile; ++q) sacc = __fadd_rn(sacc, dcur[o * kTile + q]);
+    gb[o] = __fadd_rn(gb[o], sacc);
   }
 }
 
@@ -184,31 +227,32 @@ __global__ void __launch_bounds__(kGThreads) gen_grad_kernel(GArgs g, const floa
       ain = abuf;
       __syncthreads();
       // gW[o][i] += sum_px delta[o][px] a[i][px];  gb[o] += sum_px delta[o][px]
-      float* gw = gacc + A.woff[l];
-      float* gb = gacc + A.P + A.boff[l];
-      for (int e = tid; e < fo * fi + fo; e += kGThreads) {
-        float sacc = 0.0f;
-        if (e < fo * fi) {
-          const int o = e / fi, i = e - o * fi;
-          for (int q = 0; q < kTile; ++q) sacc = fmaf(dcur[o * kTile + q], ain[i * kTile + q], sacc);
-          gw[e] = __fadd_rn(gw[e], sacc);
-        } else {
-          const int o = e - fo * fi;
-          for (int q = 0; q < kTile; ++q) sacc = __fadd_rn(sacc, dcur[o * kTile + q]);
-          gb[o] = __fadd_rn(gb[o], sacc);
-        }
-      }
+      tile_grads(dcur, ain, fi, fo, gacc + A.woff[l], gacc + A.P + A.boff[l], tid);
       if (l > 0) {
         // delta_{l-1}[i] = (sum_o delta[o] W[o][i]) * omega cos(omega z_{l-1}[i])
         float* dn = dcur == dl ? dl + A.maxw * kTile : dl;
         const float* W = ws + A.woff[l];
         const float* zl = zb + (l - 1) * A.maxw * kTile;
-        for (int i = tid >> 5; i < fi; i += kGThreads / 32) {
-          float sacc = 0.0f;
-          for (int o = 0; o < fo; ++o) sacc = fmaf(dcur[o * kTile + px], W[o * fi + i], sacc);
-          float s, c;
-          gsincos(g.acc, zl[i * kTile + px], s, c);
-          dn[i * kTile + px] = __fmul_rn(sacc, __fmul_rn(om, c));
+        const int ig = tid >> 5;
+        float sacc[kPerT];
+#pragma unroll
+        for (int k = 0; k < kPerT; ++k) sacc[k] = 0.0f;
+        for (int o = 0; o < fo; ++o) {
+          const float d = dcur[o * kTile + px];
+#pragma unroll
+          for (int k = 0; k < kPerT; ++k) {
+            const int i = ig + kGroups * k;
+            if (i < fi) sacc[k] = fmaf(d, W[o * fi + i], sacc[k]);
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < kPerT; ++k) {
+          const int i = ig + kGroups * k;
+          if (i < fi) {
+            float s, c;
+            gsincos(g.acc, zl[i * kTile + px], s, c);
+            dn[i * kTile + px] = __fmul_rn(sacc[k], __fmul_rn(om, c));
+          }
         }
         __syncthreads();
         dcur = dn;
