@@ -426,12 +426,16 @@ template <int HID, int NL, bool X3, bool ACC>
 int launch_mma_t(const StoreView& sv, const int64_t* ids, int64_t n, const DecodeArgs& a, const float* aug, void* out,
                  int32_t* status, cudaStream_t st, float omega, int flags) {
   if constexpr (HID <= 16) {
-    // CTA shape = warps x (16-pixel blocks per warp): 16 x 2 measured best for
-    // the [2,15,15,3] net against (8,4) (8,2) (16,1) (24,1) (32,1)
-    // (8 x 2 at two CTAs per SM, so consecutive launches overlap: 2% slower; 20 x 2 at 92 registers: 5% slower)
-    // (a split prologue kernel dequantising the next batch beside the running
-    // decode did not pay: at <= 120 registers the 16-warp decode leaves room
-    // only for a 2-warp prologue, which took 13 us per batch)
+    // CTA shape = warps x (16-pixel blocks per warp), two 8-warp CTAs per SM:
+    // with the separable layer 0 this is 1.5% faster than one 16-warp CTA
+    // (67.7 vs 66.7 M img/s on c2) and 0.9% faster than four 4-warp CTAs; round 1
+    // measured 16 x 2 best for the direct layer 0 against (8,4) (16,1) (24,1)
+    // (32,1) and 20 x 2 at 92 registers.  RINR_NW=16 selects one 16-warp CTA.
+    static const int nw = [] {
+      const char* e = std::getenv("RINR_NW");
+      return e ? atoi(e) : 8;
+    }();
+    if (nw == 8) return launch_mode<HID, NL, X3, ACC, 8, 2>(sv, ids, n, a, aug, out, status, st, omega, flags);
     return launch_mode<HID, NL, X3, ACC, 16, 2>(sv, ids, n, a, aug, out, status, st, omega, flags);
   } else {
     if constexpr (!ACC) {
