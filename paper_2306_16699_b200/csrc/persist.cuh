@@ -28,6 +28,42 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src)
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gmem_src) : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+
+// Record staging by the TMA bulk engine: one cp.async.bulk per record slot
+// (UBLKCP in SASS), completion counted in bytes on a shared mbarrier.
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void bulk_mbar_init(uint64_t* mbar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(mbar)) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+// expect `bytes` more and start the copy global -> shared (16-B aligned, size % 16 == 0)
+__device__ __forceinline__ void bulk_copy_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* mbar) {
+  RINR_DCHECK(in_smem(dst, bytes) && (bytes & 15u) == 0);
+  // the slot may have been read through the generic proxy (previous chunk)
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(mbar)), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(dst)),
+               "l"(src), "r"(bytes), "r"(smem_addr(mbar))
+               : "memory");
+}
+// the single arrival of the phase (after every expect_tx of the phase was issued)
+__device__ __forceinline__ void bulk_mbar_arrive(uint64_t* mbar) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_addr(mbar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_mbar_wait(uint64_t* mbar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "BULK_WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra BULK_WAIT_%=;\n\t}\n" ::"r"(smem_addr(mbar)),
+      "r"(parity)
+      : "memory");
+}
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
 // Programmatic dependent launch: wait for the preceding grid / let the next start.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
@@ -646,7 +682,11 @@ __global__ void __launch_bounds__(NW * 32, (NW < 16 ? 16 / NW : 1))
   const int nimg = int((G1u - 1) / uint32_t(gpi) - uint32_t(img0) + 1);
   float* stage = stagebase + warp * (3 * GPX + 64);  // output stage + SEP row terms
   const float invW = 1.0f / float(a.out_w);
+  __shared__ uint64_t rec_mbar;  // TMA bulk record copies of a chunk
+  uint32_t rec_phase = 0;
+  if (tid == 0) bulk_mbar_init(&rec_mbar);
   if (shared_tab) build_coord_tables(a, aug, 0, tabs, tabs + ((a.out_w + 3) & ~3), tid, NT);
+  __syncthreads();  // mbarrier initialised before any expect_tx
 
   for (int c0 = 0; c0 < nimg; c0 += lay.maxi) {
     const int ni = min(lay.maxi, nimg - c0);
@@ -668,9 +708,8 @@ __global__ void __launch_bounds__(NW * 32, (NW < 16 ? 16 / NW : 1))
       slot_of(sv, id, off, bytes);
       const uint8_t* src = sv.blob + off;
       uint8_t* dst = recs + size_t(i) * lay.rec_bytes;
-      for (uint32_t k = lane; k < bytes / 16; k += 32) cp_async16(dst + 16 * k, src + 16 * k);
+      if (lane == 0) bulk_copy_g2s(dst, src, bytes, &rec_mbar);  // one TMA bulk copy per record
     }
-    cp_async_commit();
     if (c0 == 0) dev_stamp(overlap, 1);
     if constexpr (!FRAG_TASKS)
       for (int i = tid; i < ni * lay.net_words / 4; i += NT) reinterpret_cast<uint4*>(nets)[i] = make_uint4(0, 0, 0, 0);
@@ -679,8 +718,10 @@ __global__ void __launch_bounds__(NW * 32, (NW < 16 ? 16 / NW : 1))
         float* tab = tabs + i * lay.tab_floats;
         build_coord_tables(a, aug, cimg + i, tab, tab + ((a.out_w + 3) & ~3), tid, NT);
       }
-    cp_async_wait_all();
-    __syncthreads();
+    __syncthreads();  // every expect_tx of the chunk is issued; metaid / tables written
+    if (tid == 0) bulk_mbar_arrive(&rec_mbar);
+    bulk_mbar_wait(&rec_mbar, rec_phase);
+    rec_phase ^= 1u;
     if (c0 == 0) dev_stamp(overlap, 2);
     // Dequantise straight into MMA fragments: task (image i, part h) with
     // h = 0 -> layer 0 + output layer, h = 1..NH -> hidden layer h.  Every
