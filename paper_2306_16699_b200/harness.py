@@ -11,10 +11,10 @@ Stages map onto the GPU pipeline:
   * ``clamp_convert``: 0.0, because it is fused into ``forward``.
 
 ``digest`` is sha256 over the decoded 8-bit pixels in record order, like the
-reference's.  It is deterministic from run to run.  It equals the reference's
-digest only where every u8 value does: the GPU sums in a different order, so
-a value sitting on a rounding boundary can land one level apart (at most 0.1%
-of values, tests/test_gpu_cli.py).  The throughput pass decodes all records in
+reference's.  It is deterministic from run to run and equals the reference
+harness's digest on every golden store (tests/test_gpu_digest.py); in
+general the GPU sums in a different order, so a value sitting exactly on a
+u8 rounding boundary could land one level apart.  The throughput pass decodes all records in
 batches of ``batch``.  ``jobs`` is validated, then ignored, because one launch
 covers a batch.
 """

@@ -359,6 +359,30 @@ def fitted_case():
     np.savez_compressed(OUT / "fitted.npz", **out)
 
 
+def digest_case():
+    """rinr.bench.bench digests (sha256 over the decoded u8 pixels, record
+    order, bench.py:41-73) of the golden stores, plus one sha256 per record,
+    so the GPU harness's digest can be pinned to the reference's."""
+    import hashlib
+    import tempfile
+    from rinr import bench as rbench
+    out = {}
+    for case in ("c1_r0", "c1_r1", "c2", "zoo", "fitted_A"):
+        if case == "fitted_A":
+            data = np.load(OUT / "fitted.npz")["A/archive"].tobytes()
+        else:
+            data = np.load(OUT / f"{case}.npz")["archive"].tobytes()
+        with tempfile.NamedTemporaryFile(suffix=".rinr") as f:
+            f.write(data)
+            f.flush()
+            rep = rbench.bench(f.name, batch=4)
+        out[f"{case}/digest"] = np.array(rep.digest)
+        recs = archive.read(io.BytesIO(data)).records
+        per = [hashlib.sha256(decoder.decode(r.model).as_u8().tobytes()).hexdigest() for r in recs]
+        out[f"{case}/per_record"] = np.array(per)
+    np.savez_compressed(OUT / "digests.npz", **out)
+
+
 def _src(m, h=32, w=32):
     m.source_h, m.source_w = h, w
     return m
@@ -370,8 +394,11 @@ elif __name__ == "__main__" and sys.argv[1:] == ["encoder"]:
     encoder_case()
 elif __name__ == "__main__" and sys.argv[1:] == ["fitted"]:
     fitted_case()
+elif __name__ == "__main__" and sys.argv[1:] == ["digests"]:
+    digest_case()
 elif __name__ == "__main__":
     main()
     transforms_case()
     encoder_case()
     fitted_case()
+    digest_case()

@@ -64,3 +64,40 @@ def test_bad_id_in_large_batch(c2):
     with pytest.raises(BatchItemError) as e:
         st.decode(ids, 32, 32)
     assert e.value.index == 15000
+
+
+def test_store_default_device_is_current_device():
+    """Store(device='cuda') lands on torch's current device."""
+    import torch
+    from paper_2306_16699_b200 import Store, synth
+    torch.cuda.set_device(0)
+    with Store(synth.archive_bytes(synth.config2(4, seed=1)), device="cuda") as st:
+        assert st.device.index == torch.cuda.current_device()
+        out = st.decode(torch.arange(4), 8, 8)
+        assert out.device == st.device
+
+
+def test_round2_prune_failure_is_per_image():
+    """A prune that would empty a layer fails that image alone (StructuralError
+    under on_error='skip'); the others are pruned (encoder.py:120-135)."""
+    import numpy as np
+    import torch
+    from paper_2306_16699_b200 import StructuralError, encoder, synth, transforms as T
+    mb = synth.tweak_r1(synth.random_batch(synth.ARCH_A, 3, seed=2))
+    dm = T.DeviceModels.from_batch(mb)
+    # model 1: layer 0 (30 weights) keeps a single, tiny weight -> a 0.5 global
+    # prune empties layer 0 for it only
+    m0 = dm.mask[1, :30].clone()
+    m0[:] = 0
+    m0[0] = 1
+    dm.mask[1, :30] = m0
+    dm.w[1, :30] = dm.w[1, :30] * m0.float()
+    dm.w[1, 0] = 1e-6
+    alive = [True, True, True]
+    encoder._prune_round(dm, 0.5, alive, "skip")
+    assert alive[0] is True and alive[2] is True
+    assert isinstance(alive[1], StructuralError)
+    keep = dm.mask.cpu().numpy().sum(axis=1)
+    assert keep[0] < 300 and keep[2] < 300
+    with pytest.raises(Exception):
+        encoder._prune_round(dm, 0.5, [True, True, True], "fail_fast")
