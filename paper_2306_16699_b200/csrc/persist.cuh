@@ -276,6 +276,17 @@ __device__ __forceinline__ void sep_row_terms(const SepRegs& S, float y, float* 
   rowt[slot] = __sinf(fmaf(S.w1, y, S.b1));
 }
 
+// NCHW f32 output (STORE 1) is stored straight from the output MMA's C
+// fragment: lane (g, tq) writes channel 2tq (and 2tq + 1 on tq 0) at pixels
+// g, g + 8 of each 16-pixel block; each instruction covers whole 32-byte
+// sectors (8 lanes x 4 B per channel).  8 predicated STG per group instead of
+// 8 STS + LDS.128 + STG.128 through the warp's stage.
+#ifdef RINR_STAGED_STORE1
+constexpr bool DIRECT_STORE1 = false;
+#else
+constexpr bool DIRECT_STORE1 = true;
+#endif
+
 // Per-lane store addressing, fixed for a launch.
 struct StoreLane {
   int soff[4];   // stage indices this lane reads
@@ -287,7 +298,11 @@ template <int NB, int STORE>
 __device__ __forceinline__ StoreLane make_store_lane(const DecodeArgs& a, int lane) {
   constexpr int GPX = NB * 16;
   StoreLane L{};
-  if constexpr (STORE == 1) {  // NCHW f32: lane -> (channel, float4 of the group)
+  if constexpr (STORE == 1 && DIRECT_STORE1) {  // NCHW f32 straight from the C fragment
+    const int g = lane >> 2, tq = lane & 3;
+    L.active = tq < 2;  // channels 2tq (tq 0, 1) and 2tq + 1 (tq 0)
+    L.goff = int64_t(2 * tq) * a.hw + g;
+  } else if constexpr (STORE == 1) {  // NCHW f32: lane -> (channel, float4 of the group)
     constexpr int V = GPX / 4;
     const int ch = lane / V, part = lane - ch * V;
     L.active = lane < 3 * V;
@@ -491,6 +506,27 @@ __device__ __forceinline__ void decode_group(const NetView<HID, NL>& net, const 
 #pragma unroll
       for (int e = 0; e < 4; ++e)
         ov[bk][e] = __fdiv_rn(__fsub_rn(ov[bk][e], (e & 1) ? R.mean1 : R.mean0), (e & 1) ? R.std1 : R.std0);
+  }
+  if constexpr (M::STORE == 1 && DIRECT_STORE1) {
+    if (SL.active) {
+      float* p = static_cast<float*>(out) + gofs;  // channel 2tq, pixel pbase + g
+      RINR_DCHECK(gofs >= 0 && gofs + int64_t(tq == 0 ? a.hw : 0) + 16 * (NB - 1) + 8 < a.out_elems);
+#pragma unroll
+      for (int bk = 0; bk < NB; ++bk) {
+        p[16 * bk] = ov[bk][0];
+        p[16 * bk + 8] = ov[bk][2];
+      }
+      if (tq == 0) {
+        p += a.hw;
+#pragma unroll
+        for (int bk = 0; bk < NB; ++bk) {
+          p[16 * bk] = ov[bk][1];
+          p[16 * bk + 8] = ov[bk][3];
+        }
+      }
+    }
+    __syncwarp();  // the SEP row terms written during this group become visible
+    return;
   }
 #pragma unroll
   for (int bk = 0; bk < NB; ++bk)
