@@ -103,7 +103,7 @@ __device__ __forceinline__ float sine(float x) {
 
 // Shared-memory image of one record's network, zero padded to the MMA tiles.
 //   fragH[h][t][j][lane] uint4 {b0 hi, b1 hi, b0 lo, b1 lo} of hidden layer h+1
-//   fragO[t][lane]       uint4, last layer (n-tile 0; 3 valid columns)
+//   fragO[t][lane]       uint4, last layer (n-tile 0; output c in column 2c, persist.cuh)
 //   l0[c]                float4 {omega w[c][0], omega w[c][1], omega b[c], 0}
 //   biasH[h][c]          omega * b;   scaleH[h]: f32(omega*scale) or 1
 //   modeH[h]             1 = integer-code B (affine8), 0 = float B split
@@ -193,16 +193,19 @@ __device__ __forceinline__ void build_coord_tables(const DecodeArgs& a, const fl
 // (k = 16t+2tq, +1), b1 = (k + 8, k + 9), n = 8j + g; entries outside
 // (fo, fi) are zero.  INT: integer codes (exact in bf16, lo = 0); else
 // mul * value split into bf16 hi + lo (= NetView::put_b_split).
-template <bool INT, int KIND = VK_GEN>
+// SPREAD: output row o goes to column 2o (odd columns zero), so that the C
+// fragment's first value of lane (g, tq) is output tq (persist.cuh epilogue).
+template <bool INT, int KIND = VK_GEN, bool SPREAD = false>
 __device__ __forceinline__ uint4 frag_words(const uint8_t* rec, const ValueRecipe& R, const WarpBits& B, int fi,
                                             int fo, int t, int j, float mul, int lane) {
   const int g = lane >> 2, tq = lane & 3, n = 8 * j + g;
+  const int o = SPREAD ? n >> 1 : n;
   float v[4];
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     const int k = 16 * t + 2 * tq + (q & 1) + 8 * (q >> 1);
-    const bool valid = k < fi && n < fo;
-    const float x = value_at<INT, KIND>(rec, R, B, valid ? n * fi + k : 0);
+    const bool valid = k < fi && o < fo && !(SPREAD && (n & 1));
+    const float x = value_at<INT, KIND>(rec, R, B, valid ? o * fi + k : 0);
     v[q] = valid ? (INT ? x : __fmul_rn(mul, x)) : 0.0f;
   }
   uint4 r;

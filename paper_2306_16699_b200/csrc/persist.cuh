@@ -106,21 +106,20 @@ struct ImgRegs {
   static constexpr int KR = REG_IO ? C::KT : 1;
   float4 w0[KR][4];
   uint4 bo[KR];
-  float bias_o0, bias_o1;
+  float bias_o;  // output tq's bias (output c sits in C-fragment column 2c)
   uint4 bh1[K1][N1];  // hidden layer 1 fragments (only when it is the only hidden layer)
   float2 bb1[N1];
   float sc1;
   bool int1;
-  float mean0, mean1, std0, std1;  // epilogue constants of this lane's channels (2tq, 2tq+1)
+  float mean0, std0;  // epilogue constants of this lane's channel tq (tq < 3)
   bool ident;
 
   __device__ __forceinline__ void set_norm(const DecodeArgs& a, int lane) {
     const int tq = lane & 3;
     ident = a.identity != 0;
-    mean0 = tq == 0 ? a.mean[0] : a.mean[2];
-    std0 = tq == 0 ? a.stdv[0] : a.stdv[2];
-    mean1 = a.mean[1];
-    std1 = a.stdv[1];
+    // static indices: a dynamically indexed parameter array would be copied to the stack
+    mean0 = tq == 1 ? a.mean[1] : (tq == 2 ? a.mean[2] : a.mean[0]);
+    std0 = tq == 1 ? a.stdv[1] : (tq == 2 ? a.stdv[2] : a.stdv[0]);
   }
 
   __device__ __forceinline__ void load(const NetView<HID, NL>& net, int lane) {
@@ -134,8 +133,7 @@ struct ImgRegs {
 #pragma unroll
       for (int t = 0; t < C::KT; ++t) bo[t] = reinterpret_cast<const uint4*>(net.fragO)[t * 32 + lane];
     }
-    bias_o0 = net.biasO[2 * tq];
-    bias_o1 = net.biasO[2 * tq + 1];
+    bias_o = net.biasO[tq];  // biasO[3] is zero
     if constexpr (C::NH == 1) {
 #pragma unroll
       for (int t = 0; t < C::KT; ++t)
@@ -190,7 +188,7 @@ __device__ __forceinline__ void frag_task(const StoreView& sv, const uint8_t* sl
 #pragma unroll
       for (int t = 0; t < C::KT; ++t)
         reinterpret_cast<uint4*>(net.fragO)[t * 32 + lane] =
-            frag_words<false, K>(rec, RO, BO, HID, 3, t, 0, 1.0f, lane);
+            frag_words<false, K, true>(rec, RO, BO, HID, 3, t, 0, 1.0f, lane);
     };
     const int ko = value_kind(LO);
     if (ko == VK_F32) outl(std::integral_constant<int, VK_F32>{});
@@ -277,10 +275,10 @@ __device__ __forceinline__ void sep_row_terms(const SepRegs& S, float y, float* 
 }
 
 // NCHW f32 output (STORE 1) is stored straight from the output MMA's C
-// fragment: lane (g, tq) writes channel 2tq (and 2tq + 1 on tq 0) at pixels
-// g, g + 8 of each 16-pixel block; each instruction covers whole 32-byte
-// sectors (8 lanes x 4 B per channel).  8 predicated STG per group instead of
-// 8 STS + LDS.128 + STG.128 through the warp's stage.
+// fragment: output c sits in column 2c, so lane (g, tq < 3) holds channel tq
+// at pixels g, g + 8 of each 16-pixel block and writes them with 4 STG per
+// group; each instruction covers whole 32-byte sectors (8 lanes x 4 B per
+// channel).  No stage round trip (was 8 STS + LDS.128 + STG.128).
 #ifdef RINR_STAGED_STORE1
 constexpr bool DIRECT_STORE1 = false;
 #else
@@ -300,8 +298,8 @@ __device__ __forceinline__ StoreLane make_store_lane(const DecodeArgs& a, int la
   StoreLane L{};
   if constexpr (STORE == 1 && DIRECT_STORE1) {  // NCHW f32 straight from the C fragment
     const int g = lane >> 2, tq = lane & 3;
-    L.active = tq < 2;  // channels 2tq (tq 0, 1) and 2tq + 1 (tq 0)
-    L.goff = int64_t(2 * tq) * a.hw + g;
+    L.active = tq < 3;  // channel tq
+    L.goff = int64_t(tq) * a.hw + g;
   } else if constexpr (STORE == 1) {  // NCHW f32: lane -> (channel, float4 of the group)
     constexpr int V = GPX / 4;
     const int ch = lane / V, part = lane - ch * V;
@@ -352,7 +350,7 @@ __device__ __forceinline__ void decode_group(const NetView<HID, NL>& net, const 
     const float4 r0 = reinterpret_cast<const float4*>(rowt)[tq];      // units 2tq, 2tq+1
     const float4 r1 = reinterpret_cast<const float4*>(rowt)[tq + 4];  // units 2tq+8, 2tq+9
     // next row's terms overlap this group (visible after the closing __syncwarp)
-    if (next_row) sep_row_terms(S, rowy[rb + 1], rowt_next, S.slot);
+    if (next_row) sep_row_terms(S, rowy[rb + 1 < a.out_h ? rb + 1 : rb], rowt_next, S.slot);
 #pragma unroll
     for (int bk = 0; bk < NB; ++bk) {
       float v[2][4];
@@ -480,7 +478,7 @@ __device__ __forceinline__ void decode_group(const NetView<HID, NL>& net, const 
     }
   }
   // ---- output layer + epilogue -------------------------------------------------
-  float ov[NB][4];
+  float ov[NB][2];
 #pragma unroll
   for (int bk = 0; bk < NB; ++bk) {
     // one accumulator, hi*Bhi + lo*Bhi + hi*Blo chained (no combine adds)
@@ -495,47 +493,40 @@ __device__ __forceinline__ void decode_group(const NetView<HID, NL>& net, const 
       if constexpr (X3) mma16816(o, al[bk][t], bo.x, bo.y);
       mma16816(o, ah[bk][t], bo.z, bo.w);
     }
-    // o[0]=(px g, ch 2tq) o[1]=(g, 2tq+1) o[2]=(g+8, 2tq) o[3]=(g+8, 2tq+1);
-    // bias add + clamp (decoder.py:35) in one saturating FADD
-#pragma unroll
-    for (int e = 0; e < 4; ++e) ov[bk][e] = __saturatef(o[e] + ((e & 1) ? R.bias_o1 : R.bias_o0));
+    // o[0] = (px g, column 2tq = output tq), o[2] = (px g + 8, output tq); the
+    // odd columns are zero padding.  Bias add + clamp (decoder.py:35) in one
+    // saturating FADD.
+    ov[bk][0] = __saturatef(o[0] + R.bias_o);
+    ov[bk][1] = __saturatef(o[2] + R.bias_o);
   }
   if (!R.ident) {  // one uniform branch per group
 #pragma unroll
     for (int bk = 0; bk < NB; ++bk)
 #pragma unroll
-      for (int e = 0; e < 4; ++e)
-        ov[bk][e] = __fdiv_rn(__fsub_rn(ov[bk][e], (e & 1) ? R.mean1 : R.mean0), (e & 1) ? R.std1 : R.std0);
+      for (int e = 0; e < 2; ++e) ov[bk][e] = __fdiv_rn(__fsub_rn(ov[bk][e], R.mean0), R.std0);
   }
   if constexpr (M::STORE == 1 && DIRECT_STORE1) {
     if (SL.active) {
-      float* p = static_cast<float*>(out) + gofs;  // channel 2tq, pixel pbase + g
-      RINR_DCHECK(gofs >= 0 && gofs + int64_t(tq == 0 ? a.hw : 0) + 16 * (NB - 1) + 8 < a.out_elems);
+      float* p = static_cast<float*>(out) + gofs;  // channel tq, pixel pbase + g
+      RINR_DCHECK(gofs >= 0 && gofs + 16 * (NB - 1) + 8 < a.out_elems);
 #pragma unroll
       for (int bk = 0; bk < NB; ++bk) {
         p[16 * bk] = ov[bk][0];
-        p[16 * bk + 8] = ov[bk][2];
-      }
-      if (tq == 0) {
-        p += a.hw;
-#pragma unroll
-        for (int bk = 0; bk < NB; ++bk) {
-          p[16 * bk] = ov[bk][1];
-          p[16 * bk + 8] = ov[bk][3];
-        }
+        p[16 * bk + 8] = ov[bk][1];
       }
     }
     __syncwarp();  // the SEP row terms written during this group become visible
     return;
   }
+  if (tq < 3) {
 #pragma unroll
-  for (int bk = 0; bk < NB; ++bk)
+    for (int bk = 0; bk < NB; ++bk)
 #pragma unroll
-    for (int e = 0; e < 4; ++e)
-      if (2 * tq + (e & 1) < 3) {
-        RINR_DCHECK(in_smem(stage + (2 * tq + (e & 1)) * GPX + 16 * bk + g + 8 * (e >> 1), 4));
-        stage[(2 * tq + (e & 1)) * GPX + 16 * bk + g + 8 * (e >> 1)] = ov[bk][e];
+      for (int e = 0; e < 2; ++e) {
+        RINR_DCHECK(in_smem(stage + tq * GPX + 16 * bk + g + 8 * e, 4));
+        stage[tq * GPX + 16 * bk + g + 8 * e] = ov[bk][e];
       }
+  }
   __syncwarp();
   // ---- coalesced stores -------------------------------------------------------------
   if constexpr (M::STORE == 1) {
@@ -597,18 +588,21 @@ __device__ __forceinline__ void phase2_loop(const uint32_t* nets, const float* t
   SepRegs S;
   float* rowt = stage + 3 * GPX;  // [2][32] row-term buffers (SEP)
   if constexpr (M::SEP) {
-    // out_w == GPX: group `within` is output row `within`
+    // out_w == GPX: group `within` is output row `within`.  Outer loop: one
+    // image's run of rows (setup once); inner loop: straight rows, the next
+    // row's terms computed one group ahead into the other row-term buffer.
     S.slot = sep_row_slot(lane);
+    int gg = w0g;
 #pragma unroll 1
-    for (int gg = w0g; gg < w1g; ++gg) {
-      if (i != cur) {
-        cur = i;
-        net = Net(const_cast<uint32_t*>(nets) + i * lay.net_words);
-        R.load(net, lane);
-        obase = (cimg + i) * 3 * int64_t(a.hw);
-        gofs = obase + SL.goff + int64_t(within) * GSTEP;
-        colx = shared_tab ? tabs : tabs + i * lay.tab_floats;
-        rowy = colx + ((a.out_w + 3) & ~3);
+    while (gg < w1g) {
+      const int rows = min(gpi - within, w1g - gg);
+      net = Net(const_cast<uint32_t*>(nets) + i * lay.net_words);
+      R.load(net, lane);
+      obase = (cimg + i) * 3 * int64_t(a.hw);
+      gofs = obase + SL.goff + int64_t(within) * GSTEP;
+      colx = shared_tab ? tabs : tabs + i * lay.tab_floats;
+      rowy = colx + ((a.out_w + 3) & ~3);
+      {
         const int g = lane >> 2, tq = lane & 3;
         const float4 lr = reinterpret_cast<const float4*>(net.l0)[lane & 15];
         S.w1 = lr.y;
@@ -625,18 +619,25 @@ __device__ __forceinline__ void phase2_loop(const uint32_t* nets, const float* t
               S.ca[bk][h][q] = __cosf(ax);
             }
         }
-        sep_row_terms(S, rowy[within], rowt + 32 * (gg & 1), S.slot);
-        __syncwarp();
       }
-      const bool next_row = within + 1 < gpi && gg + 1 < w1g;
-      decode_group<HID, NL, X3, ACCURATE, NB, M>(net, R, colx, rowy, a, out, cimg + i, obase, within * GPX, within,
-                                                 0, stage, SL, lane, S, rowt + 32 * (gg & 1),
-                                                 rowt + 32 * ((gg + 1) & 1), next_row, gofs);
-      gofs += GSTEP;
-      if (++within == gpi) {
-        within = 0;
-        ++i;
+      float* rc = rowt;
+      float* rn = rowt + 32;
+      sep_row_terms(S, rowy[within], rc, S.slot);
+      __syncwarp();
+      const int rend = within + rows;
+#pragma unroll 1
+      for (int r = within; r < rend; ++r) {
+        // the last row's look-ahead term (clamped index) is computed and unused
+        decode_group<HID, NL, X3, ACCURATE, NB, M>(net, R, colx, rowy, a, out, cimg + i, obase, r * GPX, r, 0,
+                                                   stage, SL, lane, S, rc, rn, true, gofs);
+        gofs += GSTEP;
+        float* t = rc;
+        rc = rn;
+        rn = t;
       }
+      gg += rows;
+      within = 0;
+      ++i;
     }
   } else {
     int rb = (within * GPX) / a.out_w, cb = within * GPX - rb * a.out_w;
@@ -826,7 +827,7 @@ __global__ void __launch_bounds__(NW * 32, (NW < 16 ? 16 / NW : 1))
       } else {
         for (int j = lane; j < L.n; j += 32) {
           const int o = j / HID, k = j - o * HID;
-          Net::put_b_split(net.fragO, 1, k, o, dq_weight(rec, L, words, words + KW, j));
+          Net::put_b_split(net.fragO, 1, k, 2 * o, dq_weight(rec, L, words, words + KW, j));  // column 2o
         }
         for (int o = lane; o < fo; o += 32) net.biasO[o] = dq_bias(rec, L, o);
       }

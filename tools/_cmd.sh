@@ -1,3 +1,2 @@
-set -x
-python -m pytest tests -m gpu -x -q -k "parity or layout or edges or digest or dropin" 2>&1 | tail -3
+python -m pytest tests -m gpu -x -q -k "parity or layout or edges or digest or dropin or fitted or zeropoint" > gpurun_out/t.log 2>&1; tail -3 gpurun_out/t.log
 bash tools/ab_bench.sh
