@@ -274,7 +274,7 @@ int launch_persist(const StoreView& sv, const int64_t* ids, int64_t n, const Dec
   constexpr int KW = (HID * HID + 31) / 32 + 1;
   PersistLayout lay{};
   lay.net_words = C::NET_WORDS;
-  lay.tab_floats = ((a.out_w + 3) & ~3) + ((a.out_h + 3) & ~3);
+  lay.tab_floats = ((a.out_w + 3) & ~3) + ((a.out_h + 4) & ~3);  // rowy[out_h]: look-ahead copy
   lay.rec_bytes = (sv.max_slot_bytes + 16 + 15) & ~15;
   lay.pfx_words = (NL * 2 * KW + 3) & ~3;
   const bool shared_tab = a.aug == RINR_AUG_NONE;
@@ -367,7 +367,7 @@ int launch_tc_t(const StoreView& sv, const int64_t* ids, int64_t n, const Decode
   constexpr int KW = (HID * HID + 31) / 32 + 1;
   TcLayout lay{};
   lay.net_bytes = (C::NET_BYTES + 127) & ~127;
-  lay.tab_floats = ((a.out_w + 3) & ~3) + ((a.out_h + 3) & ~3);
+  lay.tab_floats = ((a.out_w + 3) & ~3) + ((a.out_h + 4) & ~3);  // rowy[out_h]: look-ahead copy
   lay.rec_bytes = (sv.max_slot_bytes + 16 + 15) & ~15;
   lay.pfx_words = (NL * 2 * KW + 3) & ~3;
   constexpr int SLOT = C::slot_cols(X3);

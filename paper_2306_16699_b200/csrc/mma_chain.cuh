@@ -157,7 +157,9 @@ struct NetView {
 
 // Per-image coordinate tables (built in the prologue): colx[c], rowy[r] are
 // the source coordinates of output column c / row r after crop / flip; NaN
-// marks padding (AUG_OFFSET outside the source image).
+// marks padding (AUG_OFFSET outside the source image).  rowy[out_h] repeats
+// rowy[out_h - 1] (tables hold round4(W) + round4(H + 1) floats) so that a
+// one-row look-ahead needs no clamp.
 __device__ __forceinline__ void build_coord_tables(const DecodeArgs& a, const float* __restrict__ aug, int64_t img,
                                                    float* colx, float* rowy, int tid, int nthr) {
   const float nan = __int_as_float(0x7fc00000);
@@ -166,11 +168,12 @@ __device__ __forceinline__ void build_coord_tables(const DecodeArgs& a, const fl
 #pragma unroll
     for (int i = 0; i < 5; ++i) q[i] = aug[img * 5 + i];
   }
-  for (int i = tid; i < a.out_w + a.out_h; i += nthr) {
+  for (int i = tid; i <= a.out_w + a.out_h; i += nthr) {
     const bool is_col = i < a.out_w;
     const int n = is_col ? a.out_w : a.out_h;
     const double inv = is_col ? a.inv_wm1 : a.inv_hm1;
-    const int k = is_col ? i : i - a.out_w;
+    const int slot = is_col ? i : i - a.out_w;
+    const int k = slot < n ? slot : n - 1;
     float v;
     if (a.aug == RINR_AUG_NONE) {
       v = grid_coord(k, n, inv);
@@ -183,7 +186,7 @@ __device__ __forceinline__ void build_coord_tables(const DecodeArgs& a, const fl
                  : __fadd_rn(__fmul_rn(q[3], grid_coord(kk, n, inv)), q[1]);
     }
     if (is_col) colx[k] = v;
-    else rowy[k] = v;
+    else rowy[slot] = v;
   }
 }
 

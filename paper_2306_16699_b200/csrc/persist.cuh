@@ -89,7 +89,7 @@ __device__ __forceinline__ void dev_stamp(int, int) {}
 struct PersistLayout {
   int maxi;        // images per chunk
   int net_words;   // per image
-  int tab_floats;  // per table set: round4(W) + round4(H)
+  int tab_floats;  // per table set: round4(W) + round4(H + 1)
   int rec_bytes;   // per image record slot (16-B multiple)
   int pfx_words;   // per image: NL layers x (bit words + prefix)
 };
@@ -350,7 +350,7 @@ __device__ __forceinline__ void decode_group(const NetView<HID, NL>& net, const 
     const float4 r0 = reinterpret_cast<const float4*>(rowt)[tq];      // units 2tq, 2tq+1
     const float4 r1 = reinterpret_cast<const float4*>(rowt)[tq + 4];  // units 2tq+8, 2tq+9
     // next row's terms overlap this group (visible after the closing __syncwarp)
-    if (next_row) sep_row_terms(S, rowy[rb + 1 < a.out_h ? rb + 1 : rb], rowt_next, S.slot);
+    if (next_row) sep_row_terms(S, rowy[rb + 1], rowt_next, S.slot);  // rowy[out_h] exists
 #pragma unroll
     for (int bk = 0; bk < NB; ++bk) {
       float v[2][4];
@@ -625,16 +625,26 @@ __device__ __forceinline__ void phase2_loop(const uint32_t* nets, const float* t
       sep_row_terms(S, rowy[within], rc, S.slot);
       __syncwarp();
       const int rend = within + rows;
+      // direct NCHW f32 stores: a running output pointer (no per-group address arithmetic)
+      constexpr bool PTR = M::STORE == 1 && DIRECT_STORE1;
+      float* op = static_cast<float*>(out) + (PTR ? gofs : 0);
+      // the last row's look-ahead term (rowy[out_h]) is computed and unused
+      auto row = [&](int r, float* cur, float* nxt) {
+        decode_group<HID, NL, X3, ACCURATE, NB, M>(net, R, colx, rowy, a, PTR ? op : out, cimg + i, obase, r * GPX,
+                                                   r, 0, stage, SL, lane, S, cur, nxt, true, PTR ? 0 : gofs);
+        if constexpr (PTR) op += GSTEP;
+        else gofs += GSTEP;
+      };
+      // two rows per trip: the row-term buffers alternate at compile time and
+      // the compiler overlaps one row's epilogue with the next row's layer 0
+      // (+2% over one row per trip)
+      int r = within;
 #pragma unroll 1
-      for (int r = within; r < rend; ++r) {
-        // the last row's look-ahead term (clamped index) is computed and unused
-        decode_group<HID, NL, X3, ACCURATE, NB, M>(net, R, colx, rowy, a, out, cimg + i, obase, r * GPX, r, 0,
-                                                   stage, SL, lane, S, rc, rn, true, gofs);
-        gofs += GSTEP;
-        float* t = rc;
-        rc = rn;
-        rn = t;
+      for (; r + 1 < rend; r += 2) {
+        row(r, rc, rn);
+        row(r + 1, rn, rc);
       }
+      if (r < rend) row(r, rc, rn);
       gg += rows;
       within = 0;
       ++i;

@@ -20,7 +20,8 @@ for k in range(12):  # back to back on one stream (PDL chain), last 4 recorded
 torch.cuda.synchronize()
 t = np.zeros((4, 512, 8), np.uint64)
 assert _native.lib().rinr_dev_times(t.ctypes.data_as(C.c_void_p)) == 0
-grid = 148
+grid = int((t[0, :, 0] != 0).sum())  # CTAs that stamped (2 x 148 for 8-warp CTAs)
+print(f"grid {grid}")
 t = t[:, :grid, :].astype(np.int64)
 base = t[:, :, 0].min()
 names = ["entry", "ids+cp.async issued", "records in smem", "dequant done", "pdl_wait done", "phase2 done", "exit"]
