@@ -220,6 +220,9 @@ extern "C" RINR_API int rinr_dev_times(unsigned long long* host) {
 extern "C" RINR_API int rinr_dev_task_times(unsigned long long* host) {
   return cudaMemcpyFromSymbol(host, g_dev_task, sizeof(g_dev_task)) == cudaSuccess ? RINR_OK : RINR_ERR_CUDA;
 }
+extern "C" RINR_API int rinr_dev_tc_times(long long* host) {
+  return cudaMemcpyFromSymbol(host, g_dev_tc, sizeof(g_dev_tc)) == cudaSuccess ? RINR_OK : RINR_ERR_CUDA;
+}
 #endif
 
 int rinr_launch_dequantize(const StoreView& sv, const int64_t* d_ids, int64_t n, float* d_out, int64_t out_stride,

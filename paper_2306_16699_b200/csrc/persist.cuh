@@ -709,6 +709,13 @@ __global__ void __launch_bounds__(NW * 32, (NW < 16 ? 16 / NW : 1))
   float* stagebase = reinterpret_cast<float*>(metaid + ((lay.maxi + 1) & ~1));
 
   dev_stamp(overlap, 0);
+#ifdef RINR_DEV_KNOBS
+  if (NW <= 8 && threadIdx.x == 0 && blockIdx.x < 512) {  // SM id in the unused warp-15 task slot
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_dev_task[blockIdx.x][15][0] = smid;
+  }
+#endif
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int nblk = (a.hw + 15) / 16;
   const int gpi = (nblk + NB - 1) / NB;  // groups per image

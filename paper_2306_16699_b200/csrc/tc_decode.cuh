@@ -26,6 +26,21 @@
 #include "persist.cuh"
 
 namespace rinr {
+#ifdef RINR_DEV_KNOBS
+// Development timeline of CTA 0 (tools/dev_tc_timeline.py): clock64 of each
+// slot's issuing thread per (round, layer): [0] before the MMA wait, [1] after
+// it, [2] after the slot barrier (next A complete, MMA about to be issued),
+// [3] after the MMAs and the commit are issued.
+__device__ long long g_dev_tc[8][8][12][4];
+#define RINR_TC_STAMP(s, r, l, k)                                                        \
+  do {                                                                                   \
+    if (blockIdx.x == 0 && issuer && (r) < 8 && (l) < 12) g_dev_tc[s][r][l][k] = clock64(); \
+  } while (0)
+#else
+#define RINR_TC_STAMP(s, r, l, k) \
+  do {                            \
+  } while (0)
+#endif
 namespace tc {
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -106,6 +121,28 @@ __device__ __forceinline__ void mma_bf16_ts(uint32_t tmem_d, uint32_t tmem_a, ui
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
       "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+
+// Whole-warp forms: every lane passes the same (warp-uniform) operands and
+// elect.sync picks the issuing lane inside the asm, so the compiler needs no
+// per-thread waterfall around the uniform-datapath instruction.  Measured on
+// B200 (tools/micro/umma_lat.cu): 6 chained M128 N48 K16 MMAs + commit issue
+// in 739 cycles this way against 885 from one thread of a divergent branch.
+__device__ __forceinline__ void mma_bf16_ts_warp(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
+                                                 uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t.reg .b32 r;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync r|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void commit_warp(uint64_t* mbar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t.reg .b32 r;\n\t"
+      "elect.sync r|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}\n" ::"r"(smem_u32(mbar))
+      : "memory");
 }
 
 __device__ __forceinline__ void bar_sync(int id, int count) {
@@ -202,7 +239,13 @@ __device__ __forceinline__ void split8(const float (&x)[8], uint4& hi, uint4& lo
 }
 
 // Issue layer l's MMAs for one tile slot (l < NL-2: hidden layer l+1,
-// l == NL-2: output layer) and commit them to the slot's mbarrier.
+// l == NL-2: output layer) and commit them to the slot's mbarrier.  Called by
+// the slot's whole first warp (converged); one elected lane issues.
+#ifdef RINR_TC_THREAD_ISSUE
+constexpr bool kWarpIssue = false;
+#else
+constexpr bool kWarpIssue = true;
+#endif
 template <int HID, int NL, bool X3, bool INTB>
 __device__ __forceinline__ void issue_layer(const TcNet<HID, NL, INTB>& net, uint32_t d, int l, uint64_t* mbar) {
   using C = TcCfg<HID, NL, INTB>;
@@ -219,11 +262,16 @@ __device__ __forceinline__ void issue_layer(const TcNet<HID, NL, INTB>& net, uin
   for (int ks = 0; ks < C::KS; ++ks) {
     const uint32_t koff = uint32_t(ks * 2 * 128);  // B: two 8-element chunks per K step
     const uint32_t acol = uint32_t(ks * 8);         // A: 16 bf16 = 8 TMEM columns per K step
-    tc::mma_bf16_ts(d, ahi + acol, tc::make_desc(bhi + koff, LBO, SBO), idesc, ks > 0);
-    if (X3) tc::mma_bf16_ts(d, alo + acol, tc::make_desc(bhi + koff, LBO, SBO), idesc, 1);
-    if (!int_b) tc::mma_bf16_ts(d, ahi + acol, tc::make_desc(blo + koff, LBO, SBO), idesc, 1);
+    auto mma = [&](uint32_t a, uint64_t b, uint32_t acc) {
+      if constexpr (kWarpIssue) tc::mma_bf16_ts_warp(d, a, b, idesc, acc);
+      else tc::mma_bf16_ts(d, a, b, idesc, acc);
+    };
+    mma(ahi + acol, tc::make_desc(bhi + koff, LBO, SBO), ks > 0);
+    if (X3) mma(alo + acol, tc::make_desc(bhi + koff, LBO, SBO), 1);
+    if (!int_b) mma(ahi + acol, tc::make_desc(blo + koff, LBO, SBO), 1);
   }
-  tc::commit(mbar);
+  if constexpr (kWarpIssue) tc::commit_warp(mbar);
+  else tc::commit(mbar);
 }
 
 template <int HID, int NL, bool X3, int T, bool INTB>
@@ -424,6 +472,7 @@ __global__ void __launch_bounds__(4 * T * 32, 1)
         if (pc >= a.out_w) { pc -= a.out_w; ++pr; }
         if (pc < 0) { pc += a.out_w; --pr; }
         const float x = colx[inside ? pc : 0], y = rowy[inside ? pr : 0];
+        RINR_TC_STAMP(s, r, 0, 0);  // tile start
         // ---- layer 0 on FFMA -> A row (TMEM) ----
 #pragma unroll
         for (int ks = 0; ks < C::KS; ++ks) {
@@ -451,10 +500,14 @@ __global__ void __launch_bounds__(4 * T * 32, 1)
         tc::fence_before();
         tc::bar_sync(1 + s, 4 * 32);  // the slot's A operand is complete
         tc::fence_after();
-        if (issuer) issue_layer<HID, NL, X3, INTB>(net, dslot, 0, &mbar[s]);
+        RINR_TC_STAMP(s, r, 0, 2);
+        if (kWarpIssue ? q == 0 : issuer) issue_layer<HID, NL, X3, INTB>(net, dslot, 0, &mbar[s]);
+        RINR_TC_STAMP(s, r, 0, 3);
         // ---- hidden layers: TMEM -> sine -> A row ----
         for (int l = 0; l < NL - 2; ++l) {
+          RINR_TC_STAMP(s, r, l + 1, 0);
           tc::mbar_wait(&mbar[s], mma_phase);
+          RINR_TC_STAMP(s, r, l + 1, 1);
           mma_phase ^= 1u;
           tc::fence_after();
           const float sc = net.scaleH[l];
@@ -496,10 +549,14 @@ __global__ void __launch_bounds__(4 * T * 32, 1)
           tc::fence_before();
           tc::bar_sync(1 + s, 4 * 32);
           tc::fence_after();
-          if (issuer) issue_layer<HID, NL, X3, INTB>(net, dslot, l + 1, &mbar[s]);
+          RINR_TC_STAMP(s, r, l + 1, 2);
+          if (kWarpIssue ? q == 0 : issuer) issue_layer<HID, NL, X3, INTB>(net, dslot, l + 1, &mbar[s]);
+          RINR_TC_STAMP(s, r, l + 1, 3);
         }
         // ---- output layer ----
+        RINR_TC_STAMP(s, r, NL - 1, 0);
         tc::mbar_wait(&mbar[s], mma_phase);
+        RINR_TC_STAMP(s, r, NL - 1, 1);
         mma_phase ^= 1u;
         tc::fence_after();
         float o[8];
@@ -563,6 +620,7 @@ __global__ void __launch_bounds__(4 * T * 32, 1)
           for (int ch = 0; ch < 3; ++ch) store_value(a, out, img, p, ch, sw[ch * 32 + lane]);
         }
         __syncwarp();
+        RINR_TC_STAMP(s, r, NL, 0);  // tile stored
       }
     }
     tc::fence_before();

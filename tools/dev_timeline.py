@@ -41,3 +41,28 @@ for h in (0, 1):
     sel = d[(d >= h * 1000000) & (d < (h + 1) * 1000000)] - h * 1000000
     if sel.size:
         print(f"task h={h}: {sel.size} samples, median {np.median(sel):.0f} cycles, max {sel.max()}")
+
+# per-CTA phase 2 (pdl_wait done -> exit) against images spanned and SM
+sm = tk[:grid, 15, 0].astype(np.int64)
+gpi = 32
+total = B * gpi
+qg, rg = divmod(total, grid)
+b = np.arange(grid)
+G0 = b * qg + np.minimum(b, rg)
+G1 = G0 + qg + (b < rg)
+nimg = (G1 - 1) // gpi - G0 // gpi + 1
+for s in range(4):
+    d = (t[s][:, 6] - t[s][:, 4]) / 1e3
+    e = (t[s][:, 4] - t[s][:, 0]) / 1e3
+    print(f"slot {s}: phase2+exit p10 {np.percentile(d, 10):.2f} p50 {np.median(d):.2f} p90 {np.percentile(d, 90):.2f} max {d.max():.2f} us;"
+          f" entry->phase2 p50 {np.median(e):.2f} max {e.max():.2f}")
+    for k in sorted(set(nimg.tolist())):
+        print(f"   nimg {k}: {int((nimg == k).sum())} CTAs, phase2 mean {d[nimg == k].mean():.2f} max {d[nimg == k].max():.2f}")
+    slow = np.argsort(d)[-8:]
+    print("   slowest CTAs (cta, sm, nimg, us, entry):", [(int(c), int(sm[c]), int(nimg[c]), round(float(d[c]), 2), round(float((t[s][c, 0] - t[s][:, 0].min()) / 1e3), 2)) for c in slow])
+    # SM pairs: both CTAs of an SM
+    per_sm = {}
+    for c in range(grid):
+        per_sm.setdefault(int(sm[c]), []).append(c)
+    multi = [v for v in per_sm.values() if len(v) == 2]
+    print(f"   SMs used {len(per_sm)}; with 2 CTAs {len(multi)}")
