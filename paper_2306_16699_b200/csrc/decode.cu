@@ -282,7 +282,7 @@ int launch_persist(const StoreView& sv, const int64_t* ids, int64_t n, const Dec
   lay.pfx_words = (NL * 2 * KW + 3) & ~3;
   const bool shared_tab = a.aug == RINR_AUG_NONE;
   const size_t fixed = size_t(NW) * (3 * NB * 16 + 64) * 4 + (shared_tab ? size_t(lay.tab_floats) * 4 : 0) + 64;
-  const size_t per_img = size_t(lay.net_words) * 4 + size_t(lay.rec_bytes) + size_t(lay.pfx_words) * 4 + 8 +
+  const size_t per_img = size_t(lay.net_words) * 4 + size_t(lay.rec_bytes) + size_t(lay.pfx_words) * 4 + 16 +  // + metaid, ready
                          (shared_tab ? 0 : size_t(lay.tab_floats) * 4);
   constexpr int CPS = NW < 16 ? 16 / NW : 1;  // CTAs per SM
   const size_t budget = (228 * 1024) / CPS - 1024;

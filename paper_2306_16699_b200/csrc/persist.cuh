@@ -55,6 +55,16 @@ __device__ __forceinline__ void bulk_mbar_arrive(uint64_t* mbar) {
   asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_addr(mbar))
                : "memory");
 }
+// Per-image network readiness (phase 1 -> phase 2): count = dequant tasks of
+// the image; each task's lane 0 arrives (release) after the warp's fragment
+// writes, phase-2 warps wait (acquire) before their first group of the image.
+__device__ __forceinline__ void ready_init(uint64_t* mbar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(mbar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void ready_arrive(uint64_t* mbar) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.release.cta.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_addr(mbar))
+               : "memory");
+}
 __device__ __forceinline__ void bulk_mbar_wait(uint64_t* mbar, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred p;\n"
@@ -569,7 +579,7 @@ template <int HID, int NL, bool X3, bool ACCURATE, int NW, int NB, class M>
 __device__ __forceinline__ void phase2_loop(const uint32_t* nets, const float* tabs, const PersistLayout& lay,
                                             bool shared_tab, const DecodeArgs& a, void* __restrict__ out,
                                             int64_t cimg, int gs, int ge, int gpi, float invW, float* stage,
-                                            int warp, int lane) {
+                                            int warp, int lane, uint64_t* ready, uint32_t ready_phase) {
   using Net = NetView<HID, NL>;
   constexpr int GPX = NB * 16;
   constexpr int64_t GSTEP = M::STORE == 3 ? 3 * GPX : GPX;  // store offset advance per group (NHWC: x3)
@@ -596,6 +606,7 @@ __device__ __forceinline__ void phase2_loop(const uint32_t* nets, const float* t
 #pragma unroll 1
     while (gg < w1g) {
       const int rows = min(gpi - within, w1g - gg);
+      bulk_mbar_wait(&ready[i], ready_phase);  // image i's network is dequantised
       net = Net(const_cast<uint32_t*>(nets) + i * lay.net_words);
       R.load(net, lane);
       obase = (cimg + i) * 3 * int64_t(a.hw);
@@ -655,6 +666,7 @@ __device__ __forceinline__ void phase2_loop(const uint32_t* nets, const float* t
     for (int gg = w0g; gg < w1g; ++gg) {
       if (i != cur) {
         cur = i;
+        bulk_mbar_wait(&ready[i], ready_phase);  // image i's network is dequantised
         net = Net(const_cast<uint32_t*>(nets) + i * lay.net_words);
         R.load(net, lane);
         obase = (cimg + i) * 3 * int64_t(a.hw);
@@ -706,7 +718,8 @@ __global__ void __launch_bounds__(NW * 32, (NW < 16 ? 16 / NW : 1))
   uint8_t* recs = reinterpret_cast<uint8_t*>(tabs + (shared_tab ? 1 : lay.maxi) * lay.tab_floats);
   uint32_t* pfx = reinterpret_cast<uint32_t*>(recs + size_t(lay.maxi) * lay.rec_bytes);
   int64_t* metaid = reinterpret_cast<int64_t*>(pfx + lay.maxi * lay.pfx_words);  // [maxi]
-  float* stagebase = reinterpret_cast<float*>(metaid + ((lay.maxi + 1) & ~1));
+  uint64_t* ready = reinterpret_cast<uint64_t*>(metaid + ((lay.maxi + 1) & ~1));   // [maxi] mbarriers
+  float* stagebase = reinterpret_cast<float*>(ready + ((lay.maxi + 1) & ~1));
 
   dev_stamp(overlap, 0);
 #ifdef RINR_DEV_KNOBS
@@ -739,6 +752,11 @@ __global__ void __launch_bounds__(NW * 32, (NW < 16 ? 16 / NW : 1))
   __shared__ uint64_t rec_mbar;  // TMA bulk record copies of a chunk
   uint32_t rec_phase = 0;
   if (tid == 0) bulk_mbar_init(&rec_mbar);
+  // per-image readiness barriers, initialised once; chunk k waits on phase
+  // parity k & 1 (every image slot of a chunk receives TASKS arrivals)
+  constexpr uint32_t TASKS = FRAG_TASKS ? 1 + C::NH : NL;  // fragment-owner tasks or one per layer
+  for (int i = tid; i < lay.maxi; i += NT) ready_init(&ready[i], TASKS);
+  uint32_t ready_phase = 0;
   if (shared_tab) build_coord_tables(a, aug, 0, tabs, tabs + ((a.out_w + 3) & ~3), tid, NT);
   __syncthreads();  // mbarrier initialised before any expect_tx
 
@@ -785,19 +803,22 @@ __global__ void __launch_bounds__(NW * 32, (NW < 16 ? 16 / NW : 1))
       constexpr int TPI = 1 + C::NH;
       for (int task = (overlap & 4) ? ni * TPI : warp; task < ni * TPI; task += NW) {
         const int i = task / TPI, h = task - i * TPI;
-        if (metaid[i] < 0) continue;
+        if (metaid[i] >= 0) {
 #ifdef RINR_DEV_KNOBS
-        const unsigned long long t_a = clock64();
+          const unsigned long long t_a = clock64();
 #endif
-        frag_task<HID, NL, M::INTB>(sv, recs + size_t(i) * lay.rec_bytes, h, Net(nets + i * lay.net_words), omega,
-                                    lane);
+          frag_task<HID, NL, M::INTB>(sv, recs + size_t(i) * lay.rec_bytes, h, Net(nets + i * lay.net_words), omega,
+                                      lane);
 #ifdef RINR_DEV_KNOBS
-        __syncwarp();
-        if (lane == 0 && blockIdx.x < 512 && warp < 16 && task == warp) {
-          g_dev_task[blockIdx.x][warp][0] = t_a;
-          g_dev_task[blockIdx.x][warp][1] = clock64() - t_a + 1000000ull * h;
+          __syncwarp();
+          if (lane == 0 && blockIdx.x < 512 && warp < 16 && task == warp) {
+            g_dev_task[blockIdx.x][warp][0] = t_a;
+            g_dev_task[blockIdx.x][warp][1] = clock64() - t_a + 1000000ull * h;
+          }
+#endif
         }
-#endif
+        __syncwarp();  // the warp's fragment writes happen before lane 0's release
+        if (lane == 0) ready_arrive(&ready[i]);
       }
     }
     // Dequantise: one warp per (image, layer) task — the layer header is parsed
@@ -806,7 +827,10 @@ __global__ void __launch_bounds__(NW * 32, (NW < 16 ? 16 / NW : 1))
     if constexpr (!FRAG_TASKS)
     for (int task = (overlap & 4) ? ni * NL : warp; task < ni * NL; task += NW) {
       const int i = task / NL, l = task - i * NL;
-      if (metaid[i] < 0) continue;
+      if (metaid[i] < 0) {
+        if (lane == 0) ready_arrive(&ready[i]);
+        continue;
+      }
       const uint32_t* lo = reinterpret_cast<const uint32_t*>(recs + size_t(i) * lay.rec_bytes);
       const uint8_t* rec = recs + size_t(i) * lay.rec_bytes + sv.hdr_bytes;
       const int fi = l == 0 ? 2 : HID, fo = l == NL - 1 ? 3 : HID;
@@ -848,22 +872,30 @@ __global__ void __launch_bounds__(NW * 32, (NW < 16 ? 16 / NW : 1))
         }
         for (int o = lane; o < fo; o += 32) net.biasO[o] = dq_bias(rec, L, o);
       }
+      __syncwarp();  // the warp's writes happen before lane 0's release
+      if (lane == 0) ready_arrive(&ready[i]);
     }
-    __syncthreads();
+    if (overlap & 4) {  // RINR_DEBUG_SKIP=1 (development builds): no dequant tasks ran
+      if (tid < ni)
+        for (uint32_t k = 0; k < TASKS; ++k) ready_arrive(&ready[tid]);
+    }
     // -------------------------------- phase 2 --------------------------------
+    // No CTA barrier here: each warp starts its groups as soon as the
+    // networks of its images are ready (phase2_loop waits on `ready`).
     if (c0 == 0) {
-      dev_stamp(overlap, 3);
+      if (tid == 0) dev_stamp(overlap, 3);
       if (overlap & 1) pdl_wait();  // outputs may still be read/written by the preceding grid
       pdl_trigger();            // every CTA is resident: the next launch may start its prologue
-      dev_stamp(overlap, 4);
+      if (tid == 0) dev_stamp(overlap, 4);
     }
     const int64_t cbase = cimg * gpi;
     const int gs = int((G0 > cbase ? G0 : cbase) - cbase);
     const int ge = int((G1 < cbase + int64_t(ni) * gpi ? G1 : cbase + int64_t(ni) * gpi) - cbase);
     if (!(overlap & 2))
       phase2_loop<HID, NL, X3, ACCURATE, NW, NB, M>(nets, tabs, lay, shared_tab, a, out, cimg, gs, ge, gpi, invW,
-                                                    stage, warp, lane);
+                                                    stage, warp, lane, ready, ready_phase);
     if (c0 == 0) dev_stamp(overlap, 5);
+    ready_phase ^= 1u;
     __syncthreads();
   }
   dev_stamp(overlap, 6);
