@@ -106,6 +106,12 @@ __device__ __forceinline__ void tmem_ld8(uint32_t taddr, float (&v)[8]) {
   for (int i = 0; i < 8; ++i) v[i] = __uint_as_float(r[i]);
 }
 __device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+// Ties registers loaded by tcgen05.ld to a point after tcgen05.wait::ld (the
+// compiler may otherwise schedule their first use before the wait).
+__device__ __forceinline__ void pin8(float (&v)[8]) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) asm volatile("" : "+f"(v[i]));
+}
 __device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
                "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
@@ -514,11 +520,27 @@ __global__ void __launch_bounds__(4 * T * 32, 1)
           const float* bias = net.biasH + l * C::KP;
           constexpr int CV = (HID + 7) / 8;  // chunks holding real columns
           float v[CV][8];
+#ifdef RINR_TC_ONE_LD_WAIT
+          constexpr int CA = CV;
+#else
+          // the first K step's columns are loaded and waited for alone; the
+          // rest stay in flight while its sines run
+          constexpr int CA = CV < 2 ? CV : 2;
+#endif
 #pragma unroll
-          for (int cc = 0; cc < CV; ++cc) tc::tmem_ld8(tacc + uint32_t(cc * 8), v[cc]);
+          for (int cc = 0; cc < CA; ++cc) tc::tmem_ld8(tacc + uint32_t(cc * 8), v[cc]);
           tc::tmem_wait_ld();
 #pragma unroll
+          for (int cc = 0; cc < CA; ++cc) tc::pin8(v[cc]);
+#pragma unroll
+          for (int cc = CA; cc < CV; ++cc) tc::tmem_ld8(tacc + uint32_t(cc * 8), v[cc]);
+#pragma unroll
           for (int ks = 0; ks < C::KS; ++ks) {
+            if (ks == 1 && CA < CV) {
+              tc::tmem_wait_ld();
+#pragma unroll
+              for (int cc = CA; cc < CV; ++cc) tc::pin8(v[cc]);
+            }
             uint32_t hi[8], lo[8];
 #pragma unroll
             for (int half = 0; half < 2; ++half) {
