@@ -518,7 +518,9 @@ __device__ __forceinline__ void decode_group(const NetView<HID, NL>& net, const 
   if constexpr (M::STORE == 1 && DIRECT_STORE1) {
     if (SL.active) {
       float* p = static_cast<float*>(out) + gofs;  // channel tq, pixel pbase + g
-      RINR_DCHECK(gofs >= 0 && gofs + 16 * (NB - 1) + 8 < a.out_elems);
+      // logical element index of p[0] (the SEP loop passes a running pointer and gofs 0)
+      RINR_DCHECK(img * 3 * int64_t(a.hw) + int64_t(tq) * a.hw + pbase + g >= 0 &&
+                  img * 3 * int64_t(a.hw) + int64_t(tq) * a.hw + pbase + g + 16 * (NB - 1) + 8 < a.out_elems);
 #pragma unroll
       for (int bk = 0; bk < NB; ++bk) {
         p[16 * bk] = ov[bk][0];
