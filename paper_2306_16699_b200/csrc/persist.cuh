@@ -751,6 +751,9 @@ __global__ void __launch_bounds__(NW * 32, (NW < 16 ? 16 / NW : 1))
   const int nimg = int((G1u - 1) / uint32_t(gpi) - uint32_t(img0) + 1);
   float* stage = stagebase + warp * (3 * GPX + 64);  // output stage + SEP row terms
   const float invW = 1.0f / float(a.out_w);
+  // the first id of this warp is loaded before the setup below (its HBM
+  // latency overlaps the table build and the barrier)
+  const int64_t id_first = warp < min(lay.maxi, nimg) ? ids[img0 + warp] : 0;
   __shared__ uint64_t rec_mbar;  // TMA bulk record copies of a chunk
   uint32_t rec_phase = 0;
   if (tid == 0) bulk_mbar_init(&rec_mbar);
@@ -769,7 +772,7 @@ __global__ void __launch_bounds__(NW * 32, (NW < 16 ? 16 / NW : 1))
     // Slot copies: warp w fetches the ids of images w, w+NW, ... and streams
     // their slots into shared memory (one dependent load: the id).
     for (int i = warp; i < ni; i += NW) {
-      const int64_t id = ids[cimg + i];
+      const int64_t id = (c0 == 0 && i == warp) ? id_first : ids[cimg + i];
       const bool ok = id >= 0 && id < sv.n;
       if (c0 == 0 && i == 0 && ok) dev_stamp(overlap, 7);
       if (lane == 0) {
