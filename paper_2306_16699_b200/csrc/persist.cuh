@@ -754,16 +754,21 @@ __global__ void __launch_bounds__(NW * 32, (NW < 16 ? 16 / NW : 1))
   // the first id of this warp is loaded before the setup below (its HBM
   // latency overlaps the table build and the barrier)
   const int64_t id_first = warp < min(lay.maxi, nimg) ? ids[img0 + warp] : 0;
-  __shared__ uint64_t rec_mbar;  // TMA bulk record copies of a chunk
+  // TMA bulk record copies: one mbarrier per warp (the warp that fetches a
+  // record initialises, expects and arrives on its own barrier, so it needs
+  // no CTA barrier before issuing); chunk k completes phase parity k & 1
+  __shared__ uint64_t rec_mbar[NW];
   uint32_t rec_phase = 0;
-  if (tid == 0) bulk_mbar_init(&rec_mbar);
+  if (lane == 0) bulk_mbar_init(&rec_mbar[warp]);
+  __syncwarp();
   // per-image readiness barriers, initialised once; chunk k waits on phase
   // parity k & 1 (every image slot of a chunk receives TASKS arrivals)
   constexpr uint32_t TASKS = FRAG_TASKS ? 1 + C::NH : NL;  // fragment-owner tasks or one per layer
   for (int i = tid; i < lay.maxi; i += NT) ready_init(&ready[i], TASKS);
   uint32_t ready_phase = 0;
   if (shared_tab) build_coord_tables(a, aug, 0, tabs, tabs + ((a.out_w + 3) & ~3), tid, NT);
-  __syncthreads();  // mbarrier initialised before any expect_tx
+  // (no barrier here: the in-chunk barrier below orders the tables and the
+  // readiness barriers before any use)
 
   for (int c0 = 0; c0 < nimg; c0 += lay.maxi) {
     const int ni = min(lay.maxi, nimg - c0);
@@ -785,8 +790,9 @@ __global__ void __launch_bounds__(NW * 32, (NW < 16 ? 16 / NW : 1))
       slot_of(sv, id, off, bytes);
       const uint8_t* src = sv.blob + off;
       uint8_t* dst = recs + size_t(i) * lay.rec_bytes;
-      if (lane == 0) bulk_copy_g2s(dst, src, bytes, &rec_mbar);  // one TMA bulk copy per record
+      if (lane == 0) bulk_copy_g2s(dst, src, bytes, &rec_mbar[warp]);  // one TMA bulk copy per record
     }
+    if (lane == 0) bulk_mbar_arrive(&rec_mbar[warp]);  // after this warp's expect_tx of the chunk
     if (c0 == 0) dev_stamp(overlap, 1);
     if constexpr (!FRAG_TASKS)
       for (int i = tid; i < ni * lay.net_words / 4; i += NT) reinterpret_cast<uint4*>(nets)[i] = make_uint4(0, 0, 0, 0);
@@ -795,10 +801,7 @@ __global__ void __launch_bounds__(NW * 32, (NW < 16 ? 16 / NW : 1))
         float* tab = tabs + i * lay.tab_floats;
         build_coord_tables(a, aug, cimg + i, tab, tab + ((a.out_w + 3) & ~3), tid, NT);
       }
-    __syncthreads();  // every expect_tx of the chunk is issued; metaid / tables written
-    if (tid == 0) bulk_mbar_arrive(&rec_mbar);
-    bulk_mbar_wait(&rec_mbar, rec_phase);
-    rec_phase ^= 1u;
+    __syncthreads();  // metaid / tables / readiness barriers visible to every warp
     if (c0 == 0) dev_stamp(overlap, 2);
     // Dequantise straight into MMA fragments: task (image i, part h) with
     // h = 0 -> layer 0 + output layer, h = 1..NH -> hidden layer h.  Every
@@ -809,6 +812,7 @@ __global__ void __launch_bounds__(NW * 32, (NW < 16 ? 16 / NW : 1))
       for (int task = (overlap & 4) ? ni * TPI : warp; task < ni * TPI; task += NW) {
         const int i = task / TPI, h = task - i * TPI;
         if (metaid[i] >= 0) {
+          bulk_mbar_wait(&rec_mbar[i % NW], rec_phase);  // record i is in shared memory
 #ifdef RINR_DEV_KNOBS
           const unsigned long long t_a = clock64();
 #endif
@@ -836,6 +840,7 @@ __global__ void __launch_bounds__(NW * 32, (NW < 16 ? 16 / NW : 1))
         if (lane == 0) ready_arrive(&ready[i]);
         continue;
       }
+      bulk_mbar_wait(&rec_mbar[i % NW], rec_phase);  // record i is in shared memory
       const uint32_t* lo = reinterpret_cast<const uint32_t*>(recs + size_t(i) * lay.rec_bytes);
       const uint8_t* rec = recs + size_t(i) * lay.rec_bytes + sv.hdr_bytes;
       const int fi = l == 0 ? 2 : HID, fo = l == NL - 1 ? 3 : HID;
@@ -901,6 +906,7 @@ __global__ void __launch_bounds__(NW * 32, (NW < 16 ? 16 / NW : 1))
                                                     stage, warp, lane, ready, ready_phase);
     if (c0 == 0) dev_stamp(overlap, 5);
     ready_phase ^= 1u;
+    rec_phase ^= 1u;
     __syncthreads();
   }
   dev_stamp(overlap, 6);
