@@ -66,3 +66,18 @@ for s in range(4):
         per_sm.setdefault(int(sm[c]), []).append(c)
     multi = [v for v in per_sm.values() if len(v) == 2]
     print(f"   SMs used {len(per_sm)}; with 2 CTAs {len(multi)}")
+
+# absolute exit times (from the launch's first CTA entry) by wave and images spanned
+for s in range(4):
+    base_s = t[s][:, 0].min()
+    ex = (t[s][:, 6] - base_s) / 1e3
+    en = (t[s][:, 0] - base_s) / 1e3
+    p4 = (t[s][:, 4] - base_s) / 1e3
+    wave = (np.arange(grid) >= grid // 2).astype(int)
+    print(f"slot {s}: exit p50 {np.median(ex):.2f} p90 {np.percentile(ex, 90):.2f} max {ex.max():.2f} us")
+    for w in (0, 1):
+        for k in sorted(set(nimg.tolist())):
+            m = (wave == w) & (nimg == k)
+            if m.any():
+                print(f"   wave {w} nimg {k}: {int(m.sum())} CTAs, entry {en[m].mean():.2f}, phase2 start {p4[m].mean():.2f}, "
+                      f"exit mean {ex[m].mean():.2f} max {ex[m].max():.2f}")
