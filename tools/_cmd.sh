@@ -1,2 +1,2 @@
-python -m pytest tests -m gpu -x -q --timeout 300 -k "parity or layout or edges or digest or dropin or fuzz or accuracy" > gpurun_out/t.log 2>&1; tail -1 gpurun_out/t.log
-bash tools/ab_bench.sh
+python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" 2>&1 | tail -3
+python bench.py --impl reference --steps 3 --warmup 3 2>/dev/null | head -c 300; echo
