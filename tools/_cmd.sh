@@ -1,2 +1,1 @@
-python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" 2>&1 | tail -3
-python bench.py --impl reference --steps 3 --warmup 3 2>/dev/null | head -c 300; echo
+for f in umma_lat umma_multi umma_first; do echo "## tools/micro/$f"; timeout 120 ./tools/micro/$f; done > gpurun_out/umma.txt 2>&1; tail -3 gpurun_out/umma.txt
