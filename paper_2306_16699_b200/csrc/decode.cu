@@ -382,7 +382,7 @@ int launch_tc_t(const StoreView& sv, const int64_t* ids, int64_t n, const Decode
     r0 = size_t(maxi) * (lay.rec_bytes + size_t(lay.pfx_words) * 4);
     r0 = std::max(r0, size_t(4 * T) * 96 * 4);  // phase-2 reuse: per-warp output stage
     r0 = (r0 + 1023) & ~size_t(1023);
-    return r0 + size_t(maxi) * lay.net_bytes + size_t(shared_tab ? 1 : maxi) * lay.tab_floats * 4 + T * 8 + 16 +
+    return r0 + size_t(maxi) * lay.net_bytes + size_t(shared_tab ? 1 : maxi) * lay.tab_floats * 4 + 2 * T * 8 + 16 +
            size_t(maxi) * 8 + 64;
   };
   const int sms = num_sms();

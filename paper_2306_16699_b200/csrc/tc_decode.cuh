@@ -252,32 +252,69 @@ constexpr bool kWarpIssue = false;
 #else
 constexpr bool kWarpIssue = true;
 #endif
-template <int HID, int NL, bool X3, bool INTB>
-__device__ __forceinline__ void issue_layer(const TcNet<HID, NL, INTB>& net, uint32_t d, int l, uint64_t* mbar) {
+// Each layer's chain is committed to two mbarriers per slot.  With
+// RINR_TC_SPLITN (development option) hidden layers are issued as two
+// accumulator chains over the N halves (32 + 16 columns for N = 48), each
+// committed to its own barrier, so the epilogue could start on the first
+// columns while the tensor core computes the rest: measured 9% slower (twice
+// the MMA instructions, tools/micro/umma_lat.cu), so one chain is the default.
+#ifdef RINR_TC_SPLITN
+constexpr bool kSplitN = true;
+#else
+constexpr bool kSplitN = false;
+#endif
+template <int HID, int NL, bool INTB>
+struct SplitN {
   using C = TcCfg<HID, NL, INTB>;
-  constexpr uint32_t IDESC_H = tc::make_idesc(128, C::NP);
-  constexpr uint32_t IDESC_O = tc::make_idesc(128, C::NO);
+  static constexpr bool ON = kSplitN && C::NP > 16;
+  static constexpr int NA = ON ? (C::NP / 16 + 1) / 2 * 16 : C::NP;  // columns of the first chain
+};
+
+template <int HID, int NL, bool X3, bool INTB>
+__device__ __forceinline__ void issue_layer(const TcNet<HID, NL, INTB>& net, uint32_t d, int l, uint64_t* mb0,
+                                            uint64_t* mb1) {
+  using C = TcCfg<HID, NL, INTB>;
+  using SN = SplitN<HID, NL, INTB>;
   const uint32_t ahi = d + C::ahi_col(X3), alo = d + C::alo_col();
   const bool outl = l == NL - 2;
   const uint32_t bhi = tc::smem_u32(outl ? net.bo_hi : net.bh_hi + l * C::BH_BYTES);
   const uint32_t blo = tc::smem_u32(outl ? net.bo_lo : net.bh_lo + l * C::BH_BYTES);
-  const uint32_t idesc = outl ? IDESC_O : IDESC_H;
   const bool int_b = !outl && (INTB || net.modeH[l] != 0);
   constexpr uint32_t SBO = C::CH * 128, LBO = 128;
+  // one accumulator chain: D columns [dcol, dcol + n), B rows from brow
+  auto chain = [&](uint32_t dcol, uint32_t brow, uint32_t idesc) {
+    const uint32_t boff = (brow / 8) * SBO;
 #pragma unroll
-  for (int ks = 0; ks < C::KS; ++ks) {
-    const uint32_t koff = uint32_t(ks * 2 * 128);  // B: two 8-element chunks per K step
-    const uint32_t acol = uint32_t(ks * 8);         // A: 16 bf16 = 8 TMEM columns per K step
-    auto mma = [&](uint32_t a, uint64_t b, uint32_t acc) {
-      if constexpr (kWarpIssue) tc::mma_bf16_ts_warp(d, a, b, idesc, acc);
-      else tc::mma_bf16_ts(d, a, b, idesc, acc);
-    };
-    mma(ahi + acol, tc::make_desc(bhi + koff, LBO, SBO), ks > 0);
-    if (X3) mma(alo + acol, tc::make_desc(bhi + koff, LBO, SBO), 1);
-    if (!int_b) mma(ahi + acol, tc::make_desc(blo + koff, LBO, SBO), 1);
+    for (int ks = 0; ks < C::KS; ++ks) {
+      const uint32_t koff = boff + uint32_t(ks * 2 * 128);  // B: two 8-element chunks per K step
+      const uint32_t acol = uint32_t(ks * 8);                // A: 16 bf16 = 8 TMEM columns per K step
+      auto mma = [&](uint32_t a, uint64_t b, uint32_t acc) {
+        if constexpr (kWarpIssue) tc::mma_bf16_ts_warp(d + dcol, a, b, idesc, acc);
+        else tc::mma_bf16_ts(d + dcol, a, b, idesc, acc);
+      };
+      mma(ahi + acol, tc::make_desc(bhi + koff, LBO, SBO), ks > 0);
+      if (X3) mma(alo + acol, tc::make_desc(bhi + koff, LBO, SBO), 1);
+      if (!int_b) mma(ahi + acol, tc::make_desc(blo + koff, LBO, SBO), 1);
+    }
+  };
+  auto commit = [&](uint64_t* mb) {
+    if constexpr (kWarpIssue) tc::commit_warp(mb);
+    else tc::commit(mb);
+  };
+  if (outl) {
+    chain(0, 0, tc::make_idesc(128, C::NO));
+    commit(mb0);
+    commit(mb1);  // both barriers complete once per layer
+  } else if constexpr (SN::ON) {
+    chain(0, 0, tc::make_idesc(128, SN::NA));
+    commit(mb0);
+    chain(SN::NA, SN::NA, tc::make_idesc(128, C::NP - SN::NA));
+    commit(mb1);
+  } else {
+    chain(0, 0, tc::make_idesc(128, C::NP));
+    commit(mb0);
+    commit(mb1);
   }
-  if constexpr (kWarpIssue) tc::commit_warp(mbar);
-  else tc::commit(mbar);
 }
 
 template <int HID, int NL, bool X3, int T, bool INTB>
@@ -297,8 +334,8 @@ __global__ void __launch_bounds__(4 * T * 32, 1)
   uint8_t* nets = smem + lay.region0;                                // [maxi] networks
   float* tabs = reinterpret_cast<float*>(nets + lay.maxi * lay.net_bytes);
   const bool shared_tab = a.aug == RINR_AUG_NONE;
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(tabs + (shared_tab ? 1 : lay.maxi) * lay.tab_floats);  // [T]
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + T);
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(tabs + (shared_tab ? 1 : lay.maxi) * lay.tab_floats);  // [2T]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + 2 * T);
   int64_t* metaid = reinterpret_cast<int64_t*>(tmem_slot + 4);      // [maxi]
   uint8_t* recs = smem;  // phase-1 scratch
   uint32_t* pfx = reinterpret_cast<uint32_t*>(recs + size_t(lay.maxi) * lay.rec_bytes);
@@ -318,7 +355,7 @@ __global__ void __launch_bounds__(4 * T * 32, 1)
                  : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
-  if (tid < T) tc::mbar_init(&mbar[tid], 1);
+  if (tid < 2 * T) tc::mbar_init(&mbar[tid], 1);  // slot s: mbar[s] (first N chain), mbar[T + s]
   if (shared_tab) build_coord_tables(a, aug, 0, tabs, tabs + ((a.out_w + 3) & ~3), tid, NT);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   tc::fence_before();
@@ -507,36 +544,43 @@ __global__ void __launch_bounds__(4 * T * 32, 1)
         tc::bar_sync(1 + s, 4 * 32);  // the slot's A operand is complete
         tc::fence_after();
         RINR_TC_STAMP(s, r, 0, 2);
-        if (kWarpIssue ? q == 0 : issuer) issue_layer<HID, NL, X3, INTB>(net, dslot, 0, &mbar[s]);
+        if (kWarpIssue ? q == 0 : issuer) issue_layer<HID, NL, X3, INTB>(net, dslot, 0, &mbar[s], &mbar[T + s]);
         RINR_TC_STAMP(s, r, 0, 3);
         // ---- hidden layers: TMEM -> sine -> A row ----
         for (int l = 0; l < NL - 2; ++l) {
           RINR_TC_STAMP(s, r, l + 1, 0);
           tc::mbar_wait(&mbar[s], mma_phase);
           RINR_TC_STAMP(s, r, l + 1, 1);
-          mma_phase ^= 1u;
           tc::fence_after();
           const float sc = net.scaleH[l];
           const float* bias = net.biasH + l * C::KP;
           constexpr int CV = (HID + 7) / 8;  // chunks holding real columns
           float v[CV][8];
-#ifdef RINR_TC_ONE_LD_WAIT
-          constexpr int CA = CV;
-#else
-          // the first K step's columns are loaded and waited for alone; the
-          // rest stay in flight while its sines run
-          constexpr int CA = CV < 2 ? CV : 2;
-#endif
+          using SN = SplitN<HID, NL, INTB>;
+          // SN::ON: chunks of the first N chain, waited for on mbar[s]; the
+          // rest on mbar[T + s] once the first K steps' sines are done.
+          // Otherwise the first K step's columns are loaded and waited for
+          // alone while the rest stay in flight.
+          constexpr int CA = SN::ON ? (SN::NA / 8 < CV ? SN::NA / 8 : CV) : (CV < 2 ? CV : 2);
+          constexpr int KSA = SN::ON ? SN::NA / 16 : 1;  // K steps served by the first chunks
 #pragma unroll
           for (int cc = 0; cc < CA; ++cc) tc::tmem_ld8(tacc + uint32_t(cc * 8), v[cc]);
           tc::tmem_wait_ld();
 #pragma unroll
           for (int cc = 0; cc < CA; ++cc) tc::pin8(v[cc]);
+          if constexpr (!SN::ON) {
 #pragma unroll
-          for (int cc = CA; cc < CV; ++cc) tc::tmem_ld8(tacc + uint32_t(cc * 8), v[cc]);
+            for (int cc = CA; cc < CV; ++cc) tc::tmem_ld8(tacc + uint32_t(cc * 8), v[cc]);
+          }
 #pragma unroll
           for (int ks = 0; ks < C::KS; ++ks) {
-            if (ks == 1 && CA < CV) {
+            if (ks == KSA && CA < CV) {
+              if constexpr (SN::ON) {
+                tc::mbar_wait(&mbar[T + s], mma_phase);
+                tc::fence_after();
+#pragma unroll
+                for (int cc = CA; cc < CV; ++cc) tc::tmem_ld8(tacc + uint32_t(cc * 8), v[cc]);
+              }
               tc::tmem_wait_ld();
 #pragma unroll
               for (int cc = CA; cc < CV; ++cc) tc::pin8(v[cc]);
@@ -567,17 +611,24 @@ __global__ void __launch_bounds__(4 * T * 32, 1)
             tc::tmem_st8(tahi + uint32_t(ks * 8), hi);
             if (X3) tc::tmem_st8(talo + uint32_t(ks * 8), lo);
           }
+          if constexpr (SN::ON) {
+            if (CA >= CV) tc::mbar_wait(&mbar[T + s], mma_phase);  // keep both barriers' phases in step
+          } else {
+            tc::mbar_wait(&mbar[T + s], mma_phase);
+          }
+          mma_phase ^= 1u;
           tc::tmem_wait_st();
           tc::fence_before();
           tc::bar_sync(1 + s, 4 * 32);
           tc::fence_after();
           RINR_TC_STAMP(s, r, l + 1, 2);
-          if (kWarpIssue ? q == 0 : issuer) issue_layer<HID, NL, X3, INTB>(net, dslot, l + 1, &mbar[s]);
+          if (kWarpIssue ? q == 0 : issuer) issue_layer<HID, NL, X3, INTB>(net, dslot, l + 1, &mbar[s], &mbar[T + s]);
           RINR_TC_STAMP(s, r, l + 1, 3);
         }
         // ---- output layer ----
         RINR_TC_STAMP(s, r, NL - 1, 0);
         tc::mbar_wait(&mbar[s], mma_phase);
+        tc::mbar_wait(&mbar[T + s], mma_phase);
         RINR_TC_STAMP(s, r, NL - 1, 1);
         mma_phase ^= 1u;
         tc::fence_after();
