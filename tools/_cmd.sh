@@ -1,2 +1,2 @@
-python -m pytest tests -m gpu -x -q --timeout 300 > gpurun_out/t.log 2>&1; tail -1 gpurun_out/t.log
-bash tools/ab_bench.sh c3
+RINR_LIB_PATH=paper_2306_16699_b200/_lib_ab/librinr_b200.so python tools/dev_tc_timeline.py fp32 2>&1 | tail -7
+RINR_LIB_PATH=paper_2306_16699_b200/_lib_ab/librinr_b200.so python tools/dev_tc_timeline.py bf16 2>&1 | tail -7
