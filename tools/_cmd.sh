@@ -1,1 +1,2 @@
-RINR_NW=16 python -m pytest tests -m gpu -x -q --timeout 300 -k "parity or layout or edges or fuzz or digest" 2>&1 | tail -1
+python -m pytest tests -m gpu -x -q --timeout 300 -k "parity or layout or edges or digest or dropin or fuzz or accuracy" > gpurun_out/t.log 2>&1; tail -1 gpurun_out/t.log
+bash tools/ab_bench.sh
