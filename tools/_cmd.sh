@@ -1,2 +1,2 @@
-python -m pytest tests -m gpu -x -q --timeout 300 -k "parity or layout or edges or digest or dropin or fuzz or accuracy" > gpurun_out/t.log 2>&1; tail -1 gpurun_out/t.log
-bash tools/ab_bench.sh
+python -m pytest tests -m gpu -x -q --timeout 300 > gpurun_out/t.log 2>&1; tail -1 gpurun_out/t.log
+bash tools/ab_bench.sh c3
