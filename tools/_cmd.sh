@@ -1,1 +1,1 @@
-bash tools/ab_bench.sh
+bash tools/ab_bench.sh c3
