@@ -372,6 +372,7 @@ def measure_decode(torch, dist, cfg: str, precision: str, args, rank: int, world
     """One decode config on this rank's GPU: graph-timed value, roofline,
     clocks and (optionally) e2e through the public API."""
     from paper_2306_16699_b200.store import IMAGENET_MEAN, IMAGENET_STD, resized_crop_params
+    from paper_2306_16699_b200.trace import stage
     W = workload(cfg)
     R = args.store_records if (args.store_records and cfg == args.config) else W["records"]
     own = st is None
@@ -423,10 +424,11 @@ def measure_decode(torch, dist, cfg: str, precision: str, args, rank: int, world
         graph.replay()  # re-warm after the barrier's host round trip
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    graph.replay()
-    e1.record()
-    torch.cuda.synchronize()
+    with stage("timed"):
+        e0.record()
+        graph.replay()
+        e1.record()
+        torch.cuda.synchronize()
     elapsed = e0.elapsed_time(e1) * 1e-3
     # keep the same work running >= 1.5 s so the clock sampler sees the loaded state
     t_end = time.perf_counter() + max(0.0, 1.5 - elapsed)
@@ -489,6 +491,7 @@ def measure_decode(torch, dist, cfg: str, precision: str, args, rank: int, world
 def measure_e2e(torch, dist, st, cfg, precision, ids, aug, B, H, Wd, K, world):
     """Public API with host buffers: pinned ids in, NHWC f32 ImageBuffer batch out."""
     from paper_2306_16699_b200.store import IMAGENET_MEAN, IMAGENET_STD
+    from paper_2306_16699_b200.trace import stage
     E = min(K, 50)
     ids_host = ids[:E].cpu().pin_memory()
     p_e2e = st.decode_params(H, Wd, dtype=torch.float32, layout="nhwc", precision=precision,
@@ -535,14 +538,15 @@ def measure_e2e(torch, dist, st, cfg, precision, ids, aug, B, H, Wd, K, world):
     if dist:
         dist.barrier()
     q0, q1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    q0.record()
-    for k in range(E):
-        e2e_step(k)
-    for sl in range(2):  # the region ends when the last results are on the host
-        for c in range(2):
-            main.wait_event(copy_done[sl][c])
-    q1.record()
-    torch.cuda.synchronize()
+    with stage("e2e"):
+        q0.record()
+        for k in range(E):
+            e2e_step(k)
+        for sl in range(2):  # the region ends when the last results are on the host
+            for c in range(2):
+                main.wait_event(copy_done[sl][c])
+        q1.record()
+        torch.cuda.synchronize()
     et = reduce_max(q0.elapsed_time(q1) * 1e-3, dist, "cuda")
     return {"value": world * B * E / et, "unit": "images/s",
             "h2d_bytes_per_step": B * 8 + (B * 20 if cfg == "c3" else 0),

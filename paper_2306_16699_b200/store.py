@@ -17,6 +17,7 @@ import torch
 
 from . import _native as N
 from .errors import BatchItemError, InvalidInputError
+from .trace import stage
 
 _DTYPES = {torch.float32: N.OUT_F32, torch.bfloat16: N.OUT_BF16, torch.uint8: N.OUT_U8}
 _PREC = {"fp32": N.PREC_FP32, "bf16": N.PREC_BF16, "exact": N.PREC_EXACT}
@@ -42,8 +43,9 @@ class Store:
         self.device = dev
         arr = N.host_view(source)
         h = C.c_void_p()
-        N.check(N.lib().rinr_store_create(arr.ctypes.data if arr.size else None, arr.size, dev.index,
-                                          shard_rank, shard_world, C.byref(h)))
+        with stage("load"):
+            N.check(N.lib().rinr_store_create(arr.ctypes.data if arr.size else None, arr.size, dev.index,
+                                              shard_rank, shard_world, C.byref(h)))
         self._h = h
         info = N.StoreInfo()
         N.check(N.lib().rinr_store_info(self._h, C.byref(info)))
@@ -110,8 +112,9 @@ class Store:
         P = int(self.info.max_param_count)
         out = torch.empty((n, P), dtype=torch.float32, device=self.device)
         stream = torch.cuda.current_stream(self.device).cuda_stream
-        N.check(N.lib().rinr_dequantize(self._h, ids.data_ptr(), n, out.data_ptr(), P,
-                                        self._status.data_ptr() if check else None, stream))
+        with stage("dequantize"):
+            N.check(N.lib().rinr_dequantize(self._h, ids.data_ptr(), n, out.data_ptr(), P,
+                                            self._status.data_ptr() if check else None, stream))
         if check:
             self._raise_status(n)
         return out
@@ -166,8 +169,9 @@ class Store:
                 raise InvalidInputError(f"aug must be [n, 5], got {tuple(aug.shape)}")
             aug_ptr = aug.data_ptr()
         stream = torch.cuda.current_stream(self.device).cuda_stream
-        N.check(N.lib().rinr_decode(self._h, ids.data_ptr(), n, C.byref(params), aug_ptr, out.data_ptr(),
-                                    self._status.data_ptr() if check else None, stream))
+        with stage("forward"):
+            N.check(N.lib().rinr_decode(self._h, ids.data_ptr(), n, C.byref(params), aug_ptr, out.data_ptr(),
+                                        self._status.data_ptr() if check else None, stream))
         if check:
             self._raise_status(n)
         return out

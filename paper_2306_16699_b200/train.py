@@ -19,6 +19,7 @@ import torch
 from . import synth
 from .store import (CIFAR_MEAN, CIFAR_STD, IMAGENET_MEAN, IMAGENET_STD, Store, pad_crop_params,
                     resized_crop_params)
+from .trace import stage
 
 
 def open_sharded_store(config: str, total: int, rank: int, world: int, device="cuda", seed: int = 4242) -> Store:
@@ -83,11 +84,14 @@ class DecodeTrainLoop:
         return self.labels_all[ids]
 
     def train_on(self, x: torch.Tensor, y: torch.Tensor) -> torch.Tensor:
-        with torch.autocast(self.dev.type, dtype=torch.bfloat16, enabled=self.dev.type == "cuda"):
+        with stage("train.forward"), torch.autocast(self.dev.type, dtype=torch.bfloat16,
+                                                     enabled=self.dev.type == "cuda"):
             loss = self.lossf(self.model(x.contiguous(memory_format=torch.channels_last)), y)
         self.opt.zero_grad(set_to_none=True)
-        loss.backward()
-        self.opt.step()
+        with stage("train.backward"):  # includes DDP's bucketed gradient all-reduce
+            loss.backward()
+        with stage("train.sgd"):
+            self.opt.step()
         return loss.detach()
 
     def step(self) -> torch.Tensor:
