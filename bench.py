@@ -79,6 +79,8 @@ def parse_args(argv=None):
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-overlap", action="store_true",
                     help="do not let a decode's prologue overlap the previous decode (PDL off)")
+    ap.add_argument("--no-prefetch", action="store_true",
+                    help="do not pass the next step's ids (no L2 prefetch of the next batch's records)")
     return ap.parse_args(argv)
 
 
@@ -381,22 +383,25 @@ def measure_decode(torch, dist, cfg: str, precision: str, args, rank: int, world
     B, H, Wd = W["batch"], W["h"], W["w"]
     K, Wu = args.steps, args.warmup
     gen = torch.Generator(device="cuda").manual_seed(1 + rank)
-    ids = torch.randint(0, len(st), (Wu + K, B), device="cuda", generator=gen, dtype=torch.int64)
+    # one spare row: step k passes row k+1 as next_ids (L2 prefetch of the next batch's records)
+    ids = torch.randint(0, len(st), (Wu + K + 1, B), device="cuda", generator=gen, dtype=torch.int64)
+    pf = not args.no_prefetch
     if cfg == "c3":
         aug = [resized_crop_params(B, generator=torch.Generator().manual_seed(1000 * rank + s)).cuda()
                for s in range(Wu + K)]
         params = st.decode_params(H, Wd, dtype=torch.bfloat16, precision=precision, aug_mode="crop",
-                                  mean=IMAGENET_MEAN, std=IMAGENET_STD, overlap_prologue=not args.no_overlap)
+                                  mean=IMAGENET_MEAN, std=IMAGENET_STD, overlap_prologue=not args.no_overlap,
+                                  prefetch_next=pf)
         odt = torch.bfloat16
     else:
         aug = [None] * (Wu + K)
         params = st.decode_params(H, Wd, dtype=torch.float32, precision=precision,
-                                  overlap_prologue=not args.no_overlap)
+                                  overlap_prologue=not args.no_overlap, prefetch_next=pf)
         odt = torch.float32
     out = torch.empty((B, 3, H, Wd), dtype=odt, device="cuda")
 
     def step(k):
-        st.decode(ids[k], out=out, aug=aug[k], params=params, check=False)
+        st.decode(ids[k], out=out, aug=aug[k], params=params, check=False, next_ids=ids[k + 1] if pf else None)
 
     for k in range(Wu):
         step(k)
@@ -467,6 +472,8 @@ def measure_decode(torch, dist, cfg: str, precision: str, args, rank: int, world
                    if st.info.device_bytes > 126e6 else "store smaller than L2",
                    "parallelism": f"image-sharded x{world} (Store shard k % {world}), no decode collective",
                    "timing": "CUDA graph of K launches", "prologue_overlap": not args.no_overlap,
+                   "next_batch_prefetch": "step k passes step k+1's ids; the narrow-net kernel prefetches their "
+                   "record slots into L2 after its phase 1" if not args.no_prefetch else None,
                    "store_build_s": round(build_s, 2),
                    "store_source": "GPU generator (synth.gpu_store_bytes) -> .rinr bytes -> Store"},
         "roofline": {"bound": "mufu", "achieved": achieved / 1e9, "peak": mufu_peak / 1e9 if mufu_peak else None,

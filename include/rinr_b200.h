@@ -109,6 +109,10 @@ typedef struct {
  * while that kernel drains (programmatic dependent launch); outputs are still
  * written only after it completes. */
 #define RINR_FLAG_OVERLAP_PROLOGUE 1
+/* flags: `ids` holds 2n entries, this batch then the next one (training
+ * samplers know it); the narrow-net kernel prefetches the next batch's record
+ * slots into L2 while it decodes this one.  Output covers the first n only. */
+#define RINR_FLAG_PREFETCH_NEXT 2
 
 /* Version of this ABI (RINR_ABI_VERSION). */
 RINR_API int rinr_abi_version(void);

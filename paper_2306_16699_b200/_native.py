@@ -21,6 +21,7 @@ PREC_FP32, PREC_BF16, PREC_EXACT = 0, 1, 2
 SIN_MUFU, SIN_ACCURATE = 0, 1
 AUG_NONE, AUG_OFFSET, AUG_CROP = 0, 1, 2
 FLAG_OVERLAP_PROLOGUE = 1
+FLAG_PREFETCH_NEXT = 2
 
 EXPORTS = (
     "rinr_abi_version", "rinr_last_error", "rinr_last_error_record", "rinr_archive_validate", "rinr_archive_shard",

@@ -314,7 +314,8 @@ int launch_persist(const StoreView& sv, const int64_t* ids, int64_t n, const Dec
 #else
   constexpr int dbg = 0;
 #endif
-  int overlap = ((flags & RINR_FLAG_OVERLAP_PROLOGUE) ? 1 : 0) | (dbg << 1);
+  int overlap = ((flags & RINR_FLAG_OVERLAP_PROLOGUE) ? 1 : 0) | (dbg << 1) |
+                ((flags & RINR_FLAG_PREFETCH_NEXT) ? 64 : 0);
 #ifdef RINR_DEV_KNOBS
   static std::atomic<int> dev_slot{0};
   overlap |= (dev_slot++ & 3) << 4;  // timeline slot of this launch (dev_stamp)

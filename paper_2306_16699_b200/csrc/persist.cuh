@@ -50,6 +50,10 @@ __device__ __forceinline__ void bulk_copy_g2s(void* dst, const void* src, uint32
                "l"(src), "r"(bytes), "r"(smem_addr(mbar))
                : "memory");
 }
+// L2 prefetch of a record slot by the bulk engine (no completion tracking)
+__device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+}
 // the single arrival of the phase (after every expect_tx of the phase was issued)
 __device__ __forceinline__ void bulk_mbar_arrive(uint64_t* mbar) {
   asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(smem_addr(mbar))
@@ -754,6 +758,12 @@ __global__ void __launch_bounds__(NW * 32, (NW < 16 ? 16 / NW : 1))
   // the first id of this warp is loaded before the setup below (its HBM
   // latency overlaps the table build and the barrier)
   const int64_t id_first = warp < min(lay.maxi, nimg) ? ids[img0 + warp] : 0;
+  // RINR_FLAG_PREFETCH_NEXT (bit 64): ids[n, 2n) is the next batch; the same
+  // grid split gives this CTA the same image range there, so each warp loads
+  // one next-batch id now and prefetches its record slot into L2 after
+  // phase 1 (the id load has landed by then; the next launch's record copies
+  // then hit L2)
+  const int64_t id_next = ((overlap & 64) && warp < nimg) ? ids[int64_t(n) + img0 + warp] : -1;
   // TMA bulk record copies: one mbarrier per warp (the warp that fetches a
   // record initialises, expects and arrives on its own barrier, so it needs
   // no CTA barrier before issuing); chunk k completes phase parity k & 1
@@ -897,6 +907,12 @@ __global__ void __launch_bounds__(NW * 32, (NW < 16 ? 16 / NW : 1))
       if (overlap & 1) pdl_wait();  // outputs may still be read/written by the preceding grid
       pdl_trigger();            // every CTA is resident: the next launch may start its prologue
       if (tid == 0) dev_stamp(overlap, 4);
+      if (lane == 0 && id_next >= 0 && id_next < sv.n) {
+        uint64_t off;
+        uint32_t bytes;
+        slot_of(sv, id_next, off, bytes);
+        bulk_prefetch_l2(sv.blob + off, bytes);
+      }
     }
     const int64_t cbase = cimg * gpi;
     const int gs = int((G0 > cbase ? G0 : cbase) - cbase);

@@ -120,10 +120,13 @@ class Store:
         return out
 
     def decode_params(self, out_h, out_w, dtype=torch.float32, layout="nchw", precision="fp32", sin="mufu",
-                      aug_mode=None, mean=None, std=None, overlap_prologue: bool = False) -> N.DecodeParams:
+                      aug_mode=None, mean=None, std=None, overlap_prologue: bool = False,
+                      prefetch_next: bool = False) -> N.DecodeParams:
         """``overlap_prologue``: promise that ids/aug were not written by the
         kernel launched just before this decode on the stream, letting the
-        record fetch + dequantisation overlap that kernel's tail (PDL)."""
+        record fetch + dequantisation overlap that kernel's tail (PDL).
+        ``prefetch_next``: every decode with these params passes ``next_ids``
+        (RINR_FLAG_PREFETCH_NEXT)."""
         if out_h is None or out_w is None:
             if not self.info.uniform_source:
                 raise InvalidInputError("records differ in source size; pass out_h and out_w")
@@ -140,19 +143,34 @@ class Store:
         p.aug_mode = _AUG[aug_mode]
         p.mean[:] = list(mean) if mean is not None else [0.0, 0.0, 0.0]
         p.std[:] = list(std) if std is not None else [1.0, 1.0, 1.0]
-        p.flags = N.FLAG_OVERLAP_PROLOGUE if overlap_prologue else 0
+        p.flags = (N.FLAG_OVERLAP_PROLOGUE if overlap_prologue else 0) | (N.FLAG_PREFETCH_NEXT if prefetch_next else 0)
         return p
 
     def decode(self, ids, out_h=None, out_w=None, *, out=None, dtype=torch.float32, layout="nchw",
                precision="fp32", sin="mufu", aug=None, aug_mode=None, mean=None, std=None,
-               check=True, params=None) -> torch.Tensor:
+               check=True, params=None, next_ids=None) -> torch.Tensor:
         """Decode ``ids`` (local indices) into [n,3,H,W] (nchw) or [n,H,W,3]
         (nhwc).  ``aug``: [n,5] f32 per-image crop/flip parameters for
-        ``aug_mode`` 'offset' or 'crop' (see include/rinr_b200.h)."""
+        ``aug_mode`` 'offset' or 'crop' (see include/rinr_b200.h).
+        ``next_ids``: the next batch's n ids (already written on the device);
+        their records are prefetched into L2 during this decode.  Zero-copy
+        when they directly follow ``ids`` in memory (rows of one tensor)."""
         ids = self._ids(ids)
         n = ids.numel()
         if params is None:
-            params = self.decode_params(out_h, out_w, dtype, layout, precision, sin, aug_mode, mean, std)
+            params = self.decode_params(out_h, out_w, dtype, layout, precision, sin, aug_mode, mean, std,
+                                        prefetch_next=next_ids is not None)
+        if bool(params.flags & N.FLAG_PREFETCH_NEXT) != (next_ids is not None):
+            raise InvalidInputError("next_ids must be passed exactly when the params carry prefetch_next")
+        if next_ids is not None:
+            nxt = self._ids(next_ids)
+            if nxt.numel() != n:
+                raise InvalidInputError(f"next_ids must hold {n} ids, got {nxt.numel()}")
+            if (n and nxt.data_ptr() == ids.data_ptr() + 8 * n
+                    and nxt.untyped_storage().data_ptr() == ids.untyped_storage().data_ptr()):
+                ids = ids.as_strided((2 * n,), (1,))
+            else:
+                ids = torch.cat([ids, nxt])
         H, W = params.out_h, params.out_w
         shape = (n, 3, H, W) if params.out_layout == N.LAYOUT_NCHW else (n, H, W, 3)
         tdtype = {N.OUT_F32: torch.float32, N.OUT_BF16: torch.bfloat16, N.OUT_U8: torch.uint8}[params.out_dtype]
