@@ -31,6 +31,15 @@ def test_library_exports_header_symbols():
         assert hasattr(lib, s), s
 
 
+def test_header_constants_match_python_mirror():
+    """The enum / flag #defines of rinr_b200.h and the ctypes mirror agree."""
+    text = (ROOT / "include" / "rinr_b200.h").read_text()
+    defs = {k: int(v) for k, v in re.findall(r"#define\s+RINR_(\w+)\s+(-?\d+)\b", text)}
+    for name in ("FLAG_OVERLAP_PROLOGUE", "FLAG_PREFETCH_NEXT"):
+        assert defs[name] == getattr(N, name), name
+    assert defs["FLAG_OVERLAP_PROLOGUE"] & defs["FLAG_PREFETCH_NEXT"] == 0
+
+
 @pytest.mark.parametrize("case", STORE_CASES)
 def test_validate_golden(golden, case):
     data = golden(case)["archive"].tobytes()
